@@ -1,0 +1,153 @@
+/* tmb.h -- C ABI of the B200 Tucker-ALS (HOOI) hot path.
+ *
+ * This is the drop-in boundary for the Python API of the reference package
+ * `tmcodec` (arXiv 2104.04726 coder). Each entry point names the reference
+ * function it replaces (paths relative to /root/reference/pkg/src/tmcodec/).
+ * The reference has no compiled FFI for this path -- its boundary is the
+ * Python package surface (__init__.py:3-62) -- so the binding a maintainer
+ * adds is the ctypes shim shown in INTEGRATION.md.
+ *
+ * Conventions
+ *  - Every pointer argument named *_dev is a DEVICE pointer owned by the caller
+ *    (the library only owns a per-context workspace arena).
+ *  - Tensors are dense, F-order (mode 0 fastest): the reference linearisation
+ *    (tensor.py:1-13, DenseTensor.data tensor.py:74-78).
+ *  - Matrices (factors, Grams, eigenvectors) are column-major.
+ *  - All arithmetic accumulates in float64; tensors may be given as float32
+ *    (TMB_F32, the device format of the colour-converted stack) or float64.
+ *  - Return value: TMB_OK or an error code; tmb_last_error() has the text.
+ *    TMB_EINVAL messages reproduce the reference ValueError wording.
+ *  - A context is bound to one device and one CUDA stream; contexts are not
+ *    internally synchronised (one per host thread). Calls are stream-ordered;
+ *    functions that return host scalars synchronise the stream.
+ */
+#ifndef TMB_H_
+#define TMB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { TMB_OK = 0, TMB_EINVAL = 1, TMB_ENUMERIC = 2, TMB_ECUDA = 3, TMB_ENOTIMPL = 4 };
+enum { TMB_SPACE_RGB = 0, TMB_SPACE_YCBCR = 1, TMB_SPACE_IPT = 2 };
+enum { TMB_F32 = 0, TMB_F64 = 1 };
+enum { TMB_KIND_INIT = 0, TMB_KIND_STANDARD = 1, TMB_KIND_PP = 2 };
+
+typedef struct tmb_ctx tmb_ctx;
+
+/* SolveConfig (tucker.py:74-95); ranks are passed separately. */
+typedef struct {
+  int max_sweeps;
+  double fit_tol;
+  double pp_enter_tol;
+  double pp_exit_tol;
+  int sequential_reduction; /* 1 = ascending contraction order, 0 = greedy */
+} tmb_solve_cfg;
+
+/* SolveTrace / SweepRecord (tucker.py:98-113). Arrays are caller-owned HOST
+ * memory of length `capacity` (>= max_sweeps + 1). */
+typedef struct {
+  int capacity;
+  int n_records;
+  int converged;
+  int best_index;   /* record index of the returned model */
+  int* kind;        /* TMB_KIND_* */
+  double* fit;
+  double* max_change; /* NaN for the init record */
+} tmb_trace;
+
+/* ---- context ---------------------------------------------------------- */
+int tmb_ctx_create(int device, void* cuda_stream, tmb_ctx** out);
+int tmb_ctx_destroy(tmb_ctx* ctx);
+int tmb_ctx_set_stream(tmb_ctx* ctx, void* cuda_stream);
+const char* tmb_last_error(const tmb_ctx* ctx);
+int64_t tmb_launch_count(const tmb_ctx* ctx); /* kernels launched so far */
+int tmb_version(void);
+
+/* ---- colour (color.py) ------------------------------------------------ */
+/* n_img interleaved sRGB u8 images (h x w x 3, row-major, the PNG sample
+ * order of sceneio.read_image) -> float32 F-order tensor (h, w, 3, n_img) in
+ * the coding space: rgb_to_ycbcr (color.py:111-119) / rgb_to_ipt
+ * (color.py:145-158) of u8/255 (sceneio.py:87), stacked as in SURVEY §8.0. */
+int tmb_color_u8(tmb_ctx* ctx, const uint8_t* rgb_dev, int64_t n_img, int64_t h, int64_t w,
+                 int space, float* tensor_dev);
+/* Pixelwise float64 transforms on npx interleaved pixels (ColorImage.pixels):
+ * to_coding_space (color.py:185-194) and to_rgb (color.py:197-205). */
+int tmb_color_f64(tmb_ctx* ctx, const double* px_dev, int64_t npx, int space, double* out_dev);
+int tmb_color_inv_f64(tmb_ctx* ctx, const double* px_dev, int64_t npx, int space,
+                      double* out_dev, int64_t* n_clamped_host);
+
+/* ---- tensor kernels (tensor.py) ---------------------------------------- */
+/* ttm (tensor.py:111-123): y = x x_mode m, m column-major rows x dims[mode]. */
+int tmb_ttm(tmb_ctx* ctx, const void* x_dev, int dtype, int order, const int64_t* dims, int mode,
+            const double* m_dev, int64_t rows, double* y_dev);
+/* ttmc (tensor.py:138-173): factors[n] column-major with frows[n] x fcols[n];
+ * applied as factors[n]^T when transpose != 0. skip < 0 means none. */
+int tmb_ttmc(tmb_ctx* ctx, const void* x_dev, int dtype, int order, const int64_t* dims,
+             const double* const* factors_dev, const int64_t* frows, const int64_t* fcols,
+             int skip, int transpose, int greedy, double* y_dev);
+/* gram (tensor.py:176-180): g = m m^T for column-major rows x cols m, exactly
+ * symmetric (upper triangle computed, mirrored). */
+int tmb_gram(tmb_ctx* ctx, const double* m_dev, int64_t rows, int64_t cols, double* g_dev);
+/* gram(unfold(x, mode)) without materialising the unfolding. */
+int tmb_mode_gram(tmb_ctx* ctx, const void* x_dev, int dtype, int order, const int64_t* dims,
+                  int mode, double* g_dev);
+/* leading_eigvecs (tensor.py:183-209): dominant k eigenpairs of the symmetric
+ * n x n g, eigenvalues nonincreasing, each column sign-fixed so its first
+ * max-|entry| is positive. vecs column-major n x k. */
+int tmb_leading_eigvecs(tmb_ctx* ctx, const double* g_dev, int64_t n, int64_t k,
+                        double* vecs_dev, double* vals_dev);
+/* fro_norm^2 (tensor.py:212-214), deterministic fp64 reduction; host result. */
+int tmb_sumsq(tmb_ctx* ctx, const void* x_dev, int dtype, int64_t n, double* out_host);
+
+/* sum((t - t_hat)^2) for t (dtype) and float64 t_hat: the residual of
+ * fit(method="residual") (tucker.py:186-188); host result. */
+int tmb_resid_sumsq(tmb_ctx* ctx, const void* t_dev, int dtype, const double* that_dev, int64_t n,
+                    double* out_host);
+/* y += alpha * x (float64): the PP operand accumulation (tucker.py:268-282). */
+int tmb_axpy(tmb_ctx* ctx, int64_t n, double alpha, const double* x_dev, double* y_dev);
+
+/* ---- Tucker solver (tucker.py) ------------------------------------------ */
+/* t_hosvd (tucker.py:130-148). core F-order (ranks), factors[n] column-major. */
+int tmb_t_hosvd(tmb_ctx* ctx, const void* x_dev, int dtype, int order, const int64_t* dims,
+                const int64_t* ranks, int greedy, double* core_dev, double* const* factors_dev);
+/* hooi_sweep (tucker.py:151-163) from factors_in to factors_out (may alias). */
+int tmb_hooi_sweep(tmb_ctx* ctx, const void* x_dev, int dtype, int order, const int64_t* dims,
+                   const int64_t* ranks, const double* const* factors_in_dev, int greedy,
+                   double* core_dev, double* const* factors_out_dev);
+/* reconstruct (tucker.py:166-171): out F-order dims. */
+int tmb_reconstruct(tmb_ctx* ctx, int order, const int64_t* ranks, const int64_t* dims,
+                    const double* core_dev, const double* const* factors_dev, double* out_dev);
+/* tucker_als (tucker.py:331-397): full driver incl. trace, convergence and
+ * best-of selection. Pairwise-perturbation sweeps are not implemented yet:
+ * if a solve reaches a sweep that would run in the PP phase the call returns
+ * TMB_ENOTIMPL (never a silent divergence from the reference trace). */
+int tmb_tucker_als(tmb_ctx* ctx, const void* x_dev, int dtype, int order, const int64_t* dims,
+                   const int64_t* ranks, const tmb_solve_cfg* cfg, double* core_dev,
+                   double* const* factors_dev, tmb_trace* trace);
+
+/* ---- codec (codec.py) --------------------------------------------------- */
+/* quantize_core (codec.py:114-134): int64 levels, step returned to host. */
+int tmb_quantize_core(tmb_ctx* ctx, const double* core_dev, int64_t n, int qp,
+                      int64_t* levels_dev, double* step_host);
+/* dequantize core part (codec.py:137-148): core = levels * step. */
+int tmb_dequantize(tmb_ctx* ctx, const int64_t* levels_dev, int64_t n, double step,
+                   double* core_dev);
+
+/* ---- fused hot path ------------------------------------------------------
+ * One stack end to end: u8 images -> colour (tmb_color_u8) -> tucker_als ->
+ * quantize_core -> reconstruct + relative error ||t - t_hat|| / ||t||.
+ * tensor_dev (float32, h*w*3*n_img) receives the coding-space tensor;
+ * rel_err_host may be NULL to skip the reconstruction. */
+int tmb_encode_stack_u8(tmb_ctx* ctx, const uint8_t* rgb_dev, int64_t n_img, int64_t h, int64_t w,
+                        int space, const int64_t* ranks, const tmb_solve_cfg* cfg, int qp,
+                        float* tensor_dev, double* core_dev, double* const* factors_dev,
+                        int64_t* levels_dev, double* step_host, tmb_trace* trace,
+                        double* rel_err_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TMB_H_ */

@@ -1,0 +1,249 @@
+// Colour transforms (color.py). The hot-path kernel reads interleaved u8 sRGB
+// images and writes the coding-space tensor directly in the solver's F-order
+// layout (h fastest), transposing 32x32 pixel tiles through shared memory so
+// both the byte reads and the float writes are coalesced. It is HBM-bound:
+// 3 B read + 12 B written per pixel.
+//
+// Arithmetic is fp64 in the reference's operation order without FMA
+// contraction (__dmul_rn/__dadd_rn), then rounded once to fp32, so the Y'CbCr
+// tensor is bit-identical to fp32(reference f64 colour). The IPT path uses a
+// host-built 256-entry EOTF table (the u8 codes are exact) and CUDA pow for
+// the 0.43 power; its matrix products follow the reference's 3x3 order.
+#include "tmb_internal.cuh"
+
+namespace tmb {
+namespace {
+
+struct ColorConst {
+  double eotf[256];
+  double rgb2xyz[9];
+  double xyz2lms[9];
+  double lms2ipt[9];
+  double xyz2rgb[9];
+  double lms2xyz[9];
+  double ipt2lms[9];
+};
+__constant__ ColorConst cc;
+
+constexpr double KR = 0.299, KG = 0.587, KB = 0.114;
+
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+
+__device__ __forceinline__ void ycbcr(double r, double g, double b, double* o) {
+  // color.py:116-118
+  const double y = add(add(mul(KR, r), mul(KG, g)), mul(KB, b));
+  const double cb = add(__ddiv_rn(mul(0.5, sub(b, y)), 1.0 - KB), 0.5);
+  const double cr = add(__ddiv_rn(mul(0.5, sub(r, y)), 1.0 - KR), 0.5);
+  o[0] = fmin(fmax(y, 0.0), 1.0);
+  o[1] = fmin(fmax(cb, 0.0), 1.0);
+  o[2] = fmin(fmax(cr, 0.0), 1.0);
+}
+
+__device__ __forceinline__ void mat3(const double* m, const double* v, double* o) {
+  for (int i = 0; i < 3; ++i) o[i] = add(add(mul(v[0], m[3 * i]), mul(v[1], m[3 * i + 1])), mul(v[2], m[3 * i + 2]));
+}
+
+__device__ __forceinline__ double spow(double v, double p) {
+  // color.py:141-142 sign(v) * |v|**p
+  const double a = pow(fabs(v), p);
+  return v > 0.0 ? a : (v < 0.0 ? -a : 0.0);
+}
+
+__device__ __forceinline__ void ipt_from_lin(const double* lin, double* o) {
+  // color.py:150-158
+  double xyz[3], lms[3], lmsp[3], ipt[3];
+  mat3(cc.rgb2xyz, lin, xyz);
+  mat3(cc.xyz2lms, xyz, lms);
+  for (int i = 0; i < 3; ++i) lmsp[i] = spow(lms[i], 0.43);
+  mat3(cc.lms2ipt, lmsp, ipt);
+  o[0] = ipt[0];
+  o[1] = add(mul(0.5, ipt[1]), 0.5);
+  o[2] = add(mul(0.5, ipt[2]), 0.5);
+}
+
+__device__ __forceinline__ double eotf(double v) {
+  // color.py:131-133
+  return v > 0.04045 ? pow(__ddiv_rn(add(v, 0.055), 1.055), 2.4) : __ddiv_rn(v, 12.92);
+}
+
+__device__ __forceinline__ double oetf(double v) {
+  // color.py:136-138
+  return v > 0.0031308 ? sub(mul(1.055, pow(fmax(v, 0.0), 1.0 / 2.4)), 0.055) : mul(12.92, v);
+}
+
+// 32x32 pixel tile per block, blockDim (32, 8)
+__global__ void __launch_bounds__(256) k_color_u8(const uint8_t* __restrict__ rgb, int64_t h, int64_t w,
+                                                  int space, float* __restrict__ out) {
+  __shared__ float tile[3][32][33];  // [c][x][y]
+  const int64_t img = blockIdx.z;
+  const int64_t x0 = (int64_t)blockIdx.x * 32, y0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const uint8_t* src = rgb + img * h * w * 3;
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int64_t y = y0 + yy, x = x0 + tx;
+    if (y < h && x < w) {
+      const uint8_t* p = src + (y * w + x) * 3;
+      double o[3];
+      if (space == TMB_SPACE_YCBCR) {
+        ycbcr(__ddiv_rn((double)p[0], 255.0), __ddiv_rn((double)p[1], 255.0), __ddiv_rn((double)p[2], 255.0), o);
+      } else if (space == TMB_SPACE_IPT) {
+        const double lin[3] = {cc.eotf[p[0]], cc.eotf[p[1]], cc.eotf[p[2]]};
+        ipt_from_lin(lin, o);
+      } else {
+        o[0] = __ddiv_rn((double)p[0], 255.0); o[1] = __ddiv_rn((double)p[1], 255.0); o[2] = __ddiv_rn((double)p[2], 255.0);
+      }
+      tile[0][tx][yy] = __double2float_rn(o[0]);
+      tile[1][tx][yy] = __double2float_rn(o[1]);
+      tile[2][tx][yy] = __double2float_rn(o[2]);
+    }
+  }
+  __syncthreads();
+  float* dst = out + img * 3 * h * w;
+  for (int q = ty; q < 3 * 32; q += 8) {
+    const int ch = q / 32, xx = q % 32;
+    const int64_t x = x0 + xx, y = y0 + tx;
+    if (x < w && y < h) dst[y + h * (x + w * ch)] = tile[ch][xx][tx];
+  }
+}
+
+__global__ void k_color_f64(const double* __restrict__ px, int64_t npx, int space, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npx; i += (int64_t)gridDim.x * blockDim.x) {
+    const double r = px[3 * i], g = px[3 * i + 1], b = px[3 * i + 2];
+    double o[3];
+    if (space == TMB_SPACE_YCBCR) {
+      ycbcr(r, g, b, o);
+    } else if (space == TMB_SPACE_IPT) {
+      const double lin[3] = {eotf(r), eotf(g), eotf(b)};
+      ipt_from_lin(lin, o);
+    } else {
+      o[0] = r; o[1] = g; o[2] = b;
+    }
+    out[3 * i] = o[0]; out[3 * i + 1] = o[1]; out[3 * i + 2] = o[2];
+  }
+}
+
+// inverses (color.py:122-128, 161-182); clamp flags per pixel for ipt_to_rgb
+__global__ void k_color_inv(const double* __restrict__ px, int64_t npx, int space, double* __restrict__ out,
+                            int* __restrict__ clamped) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npx; i += (int64_t)gridDim.x * blockDim.x) {
+    const double a = px[3 * i], b = px[3 * i + 1], c = px[3 * i + 2];
+    double o[3];
+    int cl = 0;
+    if (space == TMB_SPACE_YCBCR) {
+      const double r = add(a, mul(mul(2.0, 1.0 - KR), sub(c, 0.5)));
+      const double bb = add(a, mul(mul(2.0, 1.0 - KB), sub(b, 0.5)));
+      const double g = __ddiv_rn(sub(sub(a, mul(KR, r)), mul(KB, bb)), KG);
+      o[0] = r; o[1] = g; o[2] = bb;
+    } else if (space == TMB_SPACE_IPT) {
+      const double ipt[3] = {a, mul(2.0, sub(b, 0.5)), mul(2.0, sub(c, 0.5))};
+      double lmsp[3], lms[3], xyz[3], lin[3];
+      mat3(cc.ipt2lms, ipt, lmsp);
+      for (int k = 0; k < 3; ++k) lms[k] = spow(lmsp[k], 1.0 / 0.43);
+      mat3(cc.lms2xyz, lms, xyz);
+      mat3(cc.xyz2rgb, xyz, lin);
+      for (int k = 0; k < 3; ++k) {
+        const double v = fmin(fmax(lin[k], 0.0), 1.0);
+        if (v != lin[k]) cl = 1;
+        o[k] = oetf(v);
+      }
+    } else {
+      o[0] = a; o[1] = b; o[2] = c;
+    }
+    out[3 * i] = o[0]; out[3 * i + 1] = o[1]; out[3 * i + 2] = o[2];
+    clamped[i] = cl;
+  }
+}
+
+__global__ void k_count(const int* __restrict__ f, int64_t n, unsigned long long* __restrict__ cnt) {
+  __shared__ unsigned long long s;
+  if (threadIdx.x == 0) s = 0;
+  __syncthreads();
+  unsigned long long local = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    local += f[i];
+  atomicAdd(&s, local);  // integer: order-independent
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(cnt, s);
+}
+
+// 3x3 helpers on the host (row-major), reproducing color.py:43-77
+void inv3(const double* m, double* o) {
+  const double a = m[0], b = m[1], c = m[2], d = m[3], e = m[4], f = m[5], g = m[6], h = m[7], i = m[8];
+  const double A = e * i - f * h, B = -(d * i - f * g), C = d * h - e * g;
+  const double det = a * A + b * B + c * C;
+  o[0] = A / det; o[1] = -(b * i - c * h) / det; o[2] = (b * f - c * e) / det;
+  o[3] = B / det; o[4] = (a * i - c * g) / det; o[5] = -(a * f - c * d) / det;
+  o[6] = C / det; o[7] = -(a * h - b * g) / det; o[8] = (a * e - b * d) / det;
+}
+
+bool g_const_ready[64] = {false};
+
+void ensure_constants(Ctx& c) {
+  if (c.device >= 0 && c.device < 64 && g_const_ready[c.device]) return;
+  ColorConst h{};
+  for (int v = 0; v < 256; ++v) {
+    const double x = (double)v / 255.0;
+    h.eotf[v] = x > 0.04045 ? std::pow((x + 0.055) / 1.055, 2.4) : x / 12.92;
+  }
+  const double rgb2xyz[9] = {0.4124564, 0.3575761, 0.1804375, 0.2126729, 0.7151522,
+                             0.0721750, 0.0193339, 0.1191920, 0.9503041};
+  const double hpe[9] = {0.4002, 0.7075, -0.0807, -0.2280, 1.1500, 0.0612, 0.0000, 0.0000, 0.9184};
+  double white[3];
+  for (int r = 0; r < 3; ++r) white[r] = rgb2xyz[3 * r] + rgb2xyz[3 * r + 1] + rgb2xyz[3 * r + 2];
+  for (int r = 0; r < 3; ++r) {
+    const double s = hpe[3 * r] * white[0] + hpe[3 * r + 1] * white[1] + hpe[3 * r + 2] * white[2];
+    for (int k = 0; k < 3; ++k) h.xyz2lms[3 * r + k] = hpe[3 * r + k] / s;
+  }
+  const double lms2ipt[9] = {0.4000, 0.4000, 0.2000, 4.4550, -4.8510, 0.3960, 0.8056, 0.3572, -1.1628};
+  for (int k = 0; k < 9; ++k) { h.rgb2xyz[k] = rgb2xyz[k]; h.lms2ipt[k] = lms2ipt[k]; }
+  inv3(h.rgb2xyz, h.xyz2rgb);
+  inv3(h.xyz2lms, h.lms2xyz);
+  inv3(h.lms2ipt, h.ipt2lms);
+  TMB_CUDA(cudaMemcpyToSymbol(cc, &h, sizeof(h)));
+  if (c.device >= 0 && c.device < 64) g_const_ready[c.device] = true;
+}
+
+}  // namespace
+
+void color_u8(Ctx& c, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, int space, float* out) {
+  if (n_img == 0 || h == 0 || w == 0) return;
+  ensure_constants(c);
+  dim3 grid((unsigned)ceil_div(w, 32), (unsigned)ceil_div(h, 32), (unsigned)n_img);
+  k_color_u8<<<grid, dim3(32, 8), 0, c.stream>>>(rgb, h, w, space, out);
+  c.launches++;
+  check_launch("k_color_u8");
+}
+
+void color_f64(Ctx& c, const double* px, int64_t npx, int space, double* out) {
+  if (npx == 0) return;
+  ensure_constants(c);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(npx, 256), 16LL * c.num_sms));
+  k_color_f64<<<blocks, 256, 0, c.stream>>>(px, npx, space, out);
+  c.launches++;
+  check_launch("k_color_f64");
+}
+
+void color_inv_f64(Ctx& c, const double* px, int64_t npx, int space, double* out, int64_t* n_clamped) {
+  if (npx == 0) { if (n_clamped) *n_clamped = 0; return; }
+  ensure_constants(c);
+  const size_t mk = c.arena.mark();
+  int* flags = alloc<int>(c, npx);
+  unsigned long long* cnt = alloc<unsigned long long>(c, 1);
+  TMB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), c.stream));
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(npx, 256), 16LL * c.num_sms));
+  k_color_inv<<<blocks, 256, 0, c.stream>>>(px, npx, space, out, flags);
+  c.launches++;
+  check_launch("k_color_inv");
+  k_count<<<blocks, 256, 0, c.stream>>>(flags, npx, cnt);
+  c.launches++;
+  check_launch("k_count");
+  unsigned long long hc = 0;
+  TMB_CUDA(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, c.stream));
+  TMB_CUDA(cudaStreamSynchronize(c.stream));
+  if (n_clamped) *n_clamped = (int64_t)hc;
+  c.arena.release(mk);
+}
+
+}  // namespace tmb

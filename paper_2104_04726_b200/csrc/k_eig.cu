@@ -1,0 +1,719 @@
+// Symmetric eigen-solver for leading_eigvecs (tensor.py:183-209): dominant k
+// eigenpairs, eigenvalues nonincreasing, sign rule of tensor.py:203-209.
+//
+//  n <= 64 : one-CTA cyclic Jacobi in shared memory (robust for repeated and
+//            zero eigenvalues -- the colour / exposure / view modes and the
+//            small API cases).
+//  n  > 64 : (1) Householder tridiagonalisation in ONE cooperative kernel with a
+//                single grid barrier per column (the rank-2 update of column k
+//                is fused with the symv of column k+1);
+//            (2) the top-k eigenvalues of T by 32-way multisection (one warp
+//                per eigenvalue, Sturm counts with the LAPACK pivmin guard);
+//            (3) eigenvectors of T by the twisted factorisation
+//                (T - lambda I = N_r Delta_r N_r^T, one thread per vector);
+//            (4) back-transformation x = H_0 ... H_{n-3} z in compact-WY panels
+//                of 64 reflectors (dlarft T factor + two DMMA GEMMs per panel);
+//            (5) Newton-Schulz orthonormalisation X <- X (3I - X^T X) / 2 on the
+//                DMMA GEMM, then the sign rule.
+// All fp64. Absolute accuracy is eps*||G||, the same backward error class as
+// LAPACK dsyevd that the reference calls through np.linalg.eigh.
+#include <cooperative_groups.h>
+
+#include <cfloat>
+
+#include "tmb_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace tmb {
+namespace {
+
+#define LAUNCHED(name) do { c.launches++; check_launch(name); } while (0)
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ------------------------------------------------------------------ Jacobi
+constexpr int JAC_MAX = 64;
+
+__global__ void __launch_bounds__(256) k_jacobi(const double* __restrict__ g, int n, int k,
+                                                 double* __restrict__ vecs, double* __restrict__ vals) {
+  extern __shared__ double sm[];
+  const int ld = n + 1;
+  double* A = sm;
+  double* V = A + n * ld;
+  __shared__ double cs[JAC_MAX / 2], sn[JAC_MAX / 2];
+  __shared__ int pp[JAC_MAX / 2], qq[JAC_MAX / 2];
+  __shared__ int rotated;
+  __shared__ double fro;
+  __shared__ int order[JAC_MAX];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    A[i + ld * j] = g[e];
+    V[i + ld * j] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int e = 0; e < n * n; ++e) { const double a = A[(e % n) + ld * (e / n)]; s += a * a; }
+    fro = sqrt(s);
+  }
+  __syncthreads();
+  const int np = (n + 1) & ~1;  // players incl. a bye when n is odd
+  const int half = np / 2;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int round = 0; round < np - 1; ++round) {
+      if (tid < half) {
+        auto player = [&](int pos) { return pos == 0 ? 0 : 1 + (pos - 1 + round) % (np - 1); };
+        int p = player(tid), q = player(np - 1 - tid);
+        if (p > q) { const int t = p; p = q; q = t; }
+        double c = 1.0, s = 0.0;
+        if (q < n) {
+          const double apq = A[p + ld * q], app = A[p + ld * p], aqq = A[q + ld * q];
+          const double thr = fmax(1e-17 * sqrt(fabs(app * aqq)), 1e-19 * fro);
+          if (fabs(apq) > thr) {
+            const double theta = (aqq - app) / (2.0 * apq);
+            const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            s = t * c;
+            rotated = 1;
+          }
+        }
+        pp[tid] = p; qq[tid] = q < n ? q : p; cs[tid] = c; sn[tid] = s;
+      }
+      __syncthreads();
+      // columns: A <- A J, V <- V J
+      for (int e = tid; e < half * n; e += blockDim.x) {
+        const int pr = e / n, i = e % n;
+        const int p = pp[pr], q = qq[pr];
+        if (p == q || sn[pr] == 0.0) continue;
+        const double c = cs[pr], s = sn[pr];
+        const double ap = A[i + ld * p], aq = A[i + ld * q];
+        A[i + ld * p] = c * ap - s * aq;
+        A[i + ld * q] = s * ap + c * aq;
+        const double vp = V[i + ld * p], vq = V[i + ld * q];
+        V[i + ld * p] = c * vp - s * vq;
+        V[i + ld * q] = s * vp + c * vq;
+      }
+      __syncthreads();
+      // rows: A <- J^T A
+      for (int e = tid; e < half * n; e += blockDim.x) {
+        const int pr = e / n, j = e % n;
+        const int p = pp[pr], q = qq[pr];
+        if (p == q || sn[pr] == 0.0) continue;
+        const double c = cs[pr], s = sn[pr];
+        const double ap = A[p + ld * j], aq = A[q + ld * j];
+        A[p + ld * j] = c * ap - s * aq;
+        A[q + ld * j] = s * ap + c * aq;
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  // descending order, ties by index
+  if (tid < n) {
+    const double lt = A[tid + ld * tid];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double lj = A[j + ld * j];
+      if (lj > lt || (lj == lt && j < tid)) ++rank;
+    }
+    order[rank] = tid;
+  }
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int col = warp; col < k; col += blockDim.x >> 5) {
+    const int src = order[col];
+    double best = -1.0;
+    int bi = 0;
+    for (int i = lane; i < n; i += 32) {
+      const double a = fabs(V[i + ld * src]);
+      if (a > best) { best = a; bi = i; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const double sgn = V[bi + ld * src] < 0.0 ? -1.0 : 1.0;
+    for (int i = lane; i < n; i += 32) vecs[i + (int64_t)n * col] = sgn * V[i + ld * src];
+    if (lane == 0) vals[col] = A[src + ld * src];
+  }
+}
+
+// ------------------------------------------------------------------ tridiagonalisation
+struct TrdArgs {
+  double* A;     // n x n working copy, destroyed
+  int64_t n;
+  double* d; double* e; double* tau; double* hv;  // hv: n x n, column k = v_k
+  double* pbuf;  // 2 x n
+  double* part;  // 2 x gridDim
+};
+
+__device__ double block_sum_all(double v, double* red) {
+  // result broadcast to all threads; fixed combination order
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += red[i];
+  return s;
+}
+
+// Householder for x[lo..n-1] already in buf: alpha = buf[lo], tail lo+1.. ; writes
+// v into buf (buf[lo] = 1), returns tau and beta through smem scalars.
+__device__ void house(double* buf, int64_t lo, int64_t n, double* red, double* sc) {
+  double s = 0.0;
+  for (int64_t i = lo + 1 + threadIdx.x; i < n; i += blockDim.x) s = fma(buf[i], buf[i], s);
+  const double xn2 = block_sum_all(s, red);
+  if (threadIdx.x == 0) {
+    const double alpha = buf[lo];
+    double tau = 0.0, beta = alpha, scale = 0.0;
+    if (xn2 > 0.0) {
+      const double nrm = sqrt(alpha * alpha + xn2);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    sc[0] = tau; sc[1] = beta; sc[2] = scale;
+  }
+  __syncthreads();
+  const double scale = sc[2];
+  for (int64_t i = lo + 1 + threadIdx.x; i < n; i += blockDim.x) buf[i] *= scale;  // scale=0 when tau=0
+  __syncthreads();
+  if (threadIdx.x == 0) buf[lo] = 1.0;
+  __syncthreads();
+}
+
+// One warp updates one trailing column (rows >= lo) with the pending rank-2
+// term (update == true) and returns its dot with the next reflector vn. Rows
+// are streamed in chunks of CH per lane starting at the first live row, with
+// the next chunk's loads issued before the current chunk is consumed, so the
+// L2 latency is paid about once per column and no slot below lo is touched.
+__device__ __forceinline__ double column_pass(double* __restrict__ col, int64_t lo, int64_t n, int lane,
+                                              const double* __restrict__ vk, const double* __restrict__ wk,
+                                              const double* __restrict__ vn, double vjj, double wjj, bool update) {
+  constexpr int CH = 8;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  double cur[CH], nxt[CH];
+  int64_t base = lo + lane;
+#pragma unroll
+  for (int u = 0; u < CH; ++u) cur[u] = base + 32 * u < n ? col[base + 32 * u] : 0.0;
+  while (base < n) {
+    const int64_t nb = base + 32 * CH;
+#pragma unroll
+    for (int u = 0; u < CH; ++u) nxt[u] = nb + 32 * u < n ? col[nb + 32 * u] : 0.0;
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int64_t i = base + 32 * u;
+      if (i < n) {
+        double x = cur[u];
+        if (update) {
+          x = x - vk[i] * wjj - wk[i] * vjj;
+          col[i] = x;
+        }
+        acc[u & 3] = fma(x, vn[i], acc[u & 3]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) cur[u] = nxt[u];
+    base = nb;
+  }
+  return warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+}
+
+// Deterministic block sum broadcast to every thread (fixed shuffle tree and
+// fixed warp order), identical in every block for identical inputs.
+__device__ __forceinline__ double block_sum_bcast(double v, double* red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += red[i];
+  return s;
+}
+
+constexpr int TRD_THREADS = 256;
+constexpr int TRD_PRE = 8;  // rows per thread gathered in one round trip (n <= 2048 in one go)
+
+__global__ void __launch_bounds__(TRD_THREADS, 2) k_sytrd(const TrdArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sm[];
+  const int64_t n = a.n;
+  double* vk = sm;           // current reflector v_k (rows >= k+1 valid)
+  double* wk = sm + n;       // w_k
+  double* vn = sm + 2 * n;   // next reflector v_{k+1} (rows >= k+2 valid)
+  double* red = sm + 3 * n;  // 32
+  double* sc = red + 32;     // 8
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = bd >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * nw + warp, GW = (int64_t)gridDim.x * nw;
+  double* A = a.A;
+  const int nb = gridDim.x;
+
+  // ---- prologue: reflector 0 from the original column 0, then p_0 = tau_0 A22 v_0
+  for (int64_t i = tid; i < n; i += bd) vk[i] = (i >= 1) ? A[i] : 0.0;
+  __syncthreads();
+  house(vk, 1, n, red, sc);
+  double tau_k = sc[0];
+  if (blockIdx.x == 0) {
+    if (tid == 0) { a.d[0] = A[0]; a.e[0] = sc[1]; a.tau[0] = tau_k; }
+    for (int64_t i = tid; i < n; i += bd) a.hv[i] = vk[i];
+  }
+  {
+    double wpart = 0.0;
+    for (int64_t j = 1 + gw; j < n; j += GW) {
+      const double p = tau_k * column_pass(A + n * j, 1, n, lane, vk, vk, vk, 0.0, 0.0, false);
+      if (lane == 0) a.pbuf[j] = p;
+      wpart = fma(p, vk[j], wpart);
+    }
+    const double s = block_sum_bcast(lane == 0 ? wpart : 0.0, red);
+    if (tid == 0) a.part[blockIdx.x] = s;
+  }
+  grid.sync();
+
+  for (int64_t k = 0; k + 2 < n; ++k) {
+    const int buf = (int)(k & 1);
+    const double* pb = a.pbuf + buf * n;
+    const double* pt = a.part + buf * nb;
+    const int64_t c1 = k + 1;
+    // ---- gather: partials, p_k and column c1 in one round trip
+    const double pv_part = tid < nb ? pt[tid] : 0.0;
+    const double p_c1 = pb[c1];
+    double pv[TRD_PRE], av[TRD_PRE];
+#pragma unroll
+    for (int u = 0; u < TRD_PRE; ++u) {
+      const int64_t i = c1 + tid + (int64_t)u * bd;
+      pv[u] = i < n ? pb[i] : 0.0;
+      av[u] = i < n ? A[i + n * c1] : 0.0;
+    }
+    double extra = 0.0;  // large-n tail of the partials
+    for (int b = tid + bd; b < nb; b += bd) extra += pt[b];
+    const double K = 0.5 * tau_k * block_sum_bcast(pv_part + extra, red);
+    // ---- w_k = p_k - K v_k and the updated column c1 (x) in the same pass
+    const double vj = vk[c1], wj = p_c1 - K * vj;
+    double s2 = 0.0;
+#pragma unroll
+    for (int u = 0; u < TRD_PRE; ++u) {
+      const int64_t i = c1 + tid + (int64_t)u * bd;
+      if (i < n) {
+        const double w = pv[u] - K * vk[i];
+        wk[i] = w;
+        const double x = av[u] - vk[i] * wj - w * vj;
+        if (i == c1) sc[4] = x; else vn[i] = x;
+        if (i >= k + 3) s2 = fma(x, x, s2);
+      }
+    }
+    for (int64_t i = c1 + tid + (int64_t)TRD_PRE * bd; i < n; i += bd) {
+      const double w = pb[i] - K * vk[i];
+      wk[i] = w;
+      const double x = A[i + n * c1] - vk[i] * wj - w * vj;
+      vn[i] = x;
+      s2 = fma(x, x, s2);
+    }
+    if (k + 3 == n) {  // last reflector applied: finish the 2x2 trailing block
+      __syncthreads();
+      if (blockIdx.x == 0 && tid == 0) {
+        const int64_t m = n - 2, l = n - 1;
+        a.d[m] = sc[4];
+        a.e[m] = vn[l];
+        a.d[l] = A[l + n * l] - 2.0 * vk[l] * wk[l];
+        a.tau[m] = 0.0;
+      }
+      break;
+    }
+    // ---- next reflector (redundant in every block): dlarfg on x[k+2..]
+    const double xn2 = block_sum_bcast(s2, red);
+    if (tid == 0) {
+      const double alpha = vn[k + 2];
+      double tau = 0.0, beta = alpha, scale = 0.0;
+      if (xn2 > 0.0) {
+        const double nrm = sqrt(alpha * alpha + xn2);
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      sc[0] = tau; sc[1] = beta; sc[2] = scale;
+    }
+    __syncthreads();
+    const double tau_n = sc[0], scale = sc[2];
+    for (int64_t i = k + 3 + tid; i < n; i += bd) vn[i] *= scale;
+    if (tid == 0) vn[k + 2] = 1.0;
+    __syncthreads();
+    if (blockIdx.x == 0) {
+      if (tid == 0) { a.d[c1] = sc[4]; a.e[c1] = sc[1]; a.tau[c1] = tau_n; }
+      double* h = a.hv + n * c1;
+      for (int64_t i = tid; i < n; i += bd) h[i] = (i >= k + 2) ? vn[i] : 0.0;
+    }
+    // ---- fused pass: rank-2 update of columns j >= k+2 with (v_k, w_k), then p_{k+1}
+    double* pbn = a.pbuf + (buf ^ 1) * n;
+    double wpart = 0.0;
+    for (int64_t j = k + 2 + gw; j < n; j += GW) {
+      const double p = tau_n * column_pass(A + n * j, k + 2, n, lane, vk, wk, vn, vk[j], wk[j], true);
+      if (lane == 0) pbn[j] = p;
+      wpart = fma(p, vn[j], wpart);
+    }
+    const double s = block_sum_bcast(lane == 0 ? wpart : 0.0, red);
+    if (tid == 0) a.part[(buf ^ 1) * nb + blockIdx.x] = s;
+    // v_k <- v_{k+1}: swap buffers (rows below k+2 are never read again)
+    double* t = vk; vk = vn; vn = t;
+    tau_k = tau_n;
+    grid.sync();
+  }
+}
+
+// ------------------------------------------------------------------ bisection
+__device__ __forceinline__ int sturm_count(const double* __restrict__ d, const double* __restrict__ e,
+                                           int64_t n, double x, double pivmin) {
+  double q = d[0] - x;
+  if (fabs(q) <= pivmin) q = -pivmin;
+  int cnt = q < 0.0;
+  for (int64_t i = 1; i < n; ++i) {
+    const double ei = e[i - 1];
+    q = (d[i] - x) - ei * ei / q;
+    if (fabs(q) <= pivmin) q = -pivmin;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+__global__ void k_bisect(const double* __restrict__ d, const double* __restrict__ e, int64_t n, int64_t k,
+                         double* __restrict__ vals) {
+  const int lane = threadIdx.x & 31;
+  const int64_t jd = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (jd >= k) return;
+  const int64_t ja = n - 1 - jd;  // ascending index
+  // Gershgorin bounds and pivmin (every warp redundantly; O(n))
+  double gl = 1e308, gu = -1e308, emax2 = 0.0;
+  for (int64_t i = lane; i < n; i += 32) {
+    const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
+    gl = fmin(gl, d[i] - r);
+    gu = fmax(gu, d[i] + r);
+    if (i + 1 < n) emax2 = fmax(emax2, e[i] * e[i]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+    gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+    emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
+  }
+  const double pivmin = DBL_MIN * fmax(1.0, emax2);
+  const double span = fmax(gu - gl, fmax(fabs(gl), fabs(gu)) * DBL_EPSILON);
+  double lo = gl - 2.0 * DBL_EPSILON * span - 2.0 * pivmin;
+  double hi = gu + 2.0 * DBL_EPSILON * span + 2.0 * pivmin;
+  for (int round = 0; round < 24; ++round) {
+    const double w = hi - lo;
+    // absolute accuracy eps*||T|| (Sturm counts resolve nothing finer)
+    if (w <= 2.0 * DBL_EPSILON * fmax(fabs(gl), fabs(gu)) + 4.0 * pivmin) break;
+    const double x = lo + w * (double)(lane + 1) / 33.0;
+    const int c = sturm_count(d, e, n, x, pivmin);
+    const unsigned above = __ballot_sync(0xffffffffu, c > ja);  // eigenvalue ja < x
+    const int first = above ? __ffs(above) - 1 : 32;
+    const double xf = __shfl_sync(0xffffffffu, x, first < 32 ? first : 31);
+    const double xp = __shfl_sync(0xffffffffu, x, first > 0 ? first - 1 : 0);
+    if (first == 32) lo = xf;            // all counts <= ja: eigenvalue above x_31
+    else { hi = xf; if (first > 0) lo = xp; }
+  }
+  if (lane == 0) vals[jd] = 0.5 * (lo + hi);
+}
+
+// ------------------------------------------------------------------ twisted factorisation
+// z (unnormalised) for eigenvalue vals[j]; scratch dp/dm laid out [i][j] for coalescing.
+__global__ void k_twisted(const double* __restrict__ d, const double* __restrict__ e, int64_t n, int64_t k,
+                          const double* __restrict__ vals, double* __restrict__ dp, double* __restrict__ dm,
+                          double* __restrict__ zrow) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= k) return;
+  const double lam = vals[j];
+  double emax2 = 0.0;
+  for (int64_t i = 0; i + 1 < n; ++i) emax2 = fmax(emax2, e[i] * e[i]);
+  const double pivmin = DBL_MIN * fmax(1.0, emax2);
+  // stationary (top-down) D+
+  double q = d[0] - lam;
+  if (fabs(q) <= pivmin) q = -pivmin;
+  dp[j] = q;
+  for (int64_t i = 1; i < n; ++i) {
+    const double ei = e[i - 1];
+    q = (d[i] - lam) - ei * ei / q;
+    if (fabs(q) <= pivmin) q = -pivmin;
+    dp[i * k + j] = q;
+  }
+  // progressive (bottom-up) D-, twist index r = argmin |gamma|
+  double m = d[n - 1] - lam;
+  if (fabs(m) <= pivmin) m = -pivmin;
+  dm[(n - 1) * k + j] = m;
+  int64_t r = n - 1;
+  double gbest = fabs(dp[(n - 1) * k + j]);  // gamma_{n-1} = D+_{n-1}
+  for (int64_t i0 = n - 2; i0 >= 0; i0 -= 8) {
+    double dpv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) dpv[u] = i0 - u >= 0 ? dp[(i0 - u) * k + j] : 0.0;  // prefetch
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 - u;
+      if (i < 0) break;
+      const double ei = e[i];
+      const double t = (d[i] - lam) - ei * ei / m;
+      m = fabs(t) <= pivmin ? -pivmin : t;
+      dm[i * k + j] = m;
+      const double gamma = dpv[u] + m - (d[i] - lam);
+      if (fabs(gamma) < gbest) { gbest = fabs(gamma); r = i; }
+    }
+  }
+  // z_r = 1, outward recurrences; the ratios do not depend on z, so they are
+  // computed 8 at a time ahead of the multiply chain.
+  zrow[r * k + j] = 1.0;
+  constexpr int U = 8;
+  double z = 1.0;
+  for (int64_t i0 = r - 1; i0 >= 0; i0 -= U) {
+    double rt[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 - u;
+      rt[u] = i >= 0 ? -(e[i] / dp[i * k + j]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 - u;
+      if (i >= 0) {
+        z = rt[u] * z;
+        if (!(fabs(z) < 1e280)) z = (z > 0 ? 1e280 : -1e280);
+        zrow[i * k + j] = z;
+      }
+    }
+  }
+  z = 1.0;
+  for (int64_t i0 = r + 1; i0 < n; i0 += U) {
+    double rt[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u;
+      rt[u] = i < n ? -(e[i - 1] / dm[i * k + j]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u;
+      if (i < n) {
+        z = rt[u] * z;
+        if (!(fabs(z) < 1e280)) z = (z > 0 ? 1e280 : -1e280);
+        zrow[i * k + j] = z;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ back-transformation
+// z (row layout [i][j]) -> x (column-major), each column scaled to unit norm.
+__global__ void k_znorm(const double* __restrict__ zrow, int64_t n, int64_t k, double* __restrict__ x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= k) return;
+  double mx = 0.0;
+  for (int64_t i = lane; i < n; i += 32) mx = fmax(mx, fabs(zrow[i * k + j]));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const double inv = mx > 0.0 ? 1.0 / mx : 1.0;
+  double s = 0.0;
+  for (int64_t i = lane; i < n; i += 32) { const double v = zrow[i * k + j] * inv; s = fma(v, v, s); }
+  const double nrm = inv / sqrt(warp_sum(s));
+  for (int64_t i = lane; i < n; i += 32) x[i + n * j] = zrow[i * k + j] * nrm;
+}
+
+// Compact-WY T factor of one panel of nb forward reflectors (LAPACK dlarft):
+// H_0 ... H_{nb-1} = I - V T V^T, T(i,i) = tau_i,
+// T(0:i, i) = -tau_i T(0:i, 0:i) S(0:i, i) with S = V^T V.
+__global__ void k_larft(const double* __restrict__ S, const double* __restrict__ tau, int nb,
+                        double* __restrict__ T) {
+  extern __shared__ double sT[];  // nb x nb column-major
+  const int p = blockIdx.x, r = threadIdx.x;
+  const double* Sp = S + (int64_t)p * nb * nb;
+  const double* tp = tau + (int64_t)p * nb;
+  for (int i = 0; i < nb; ++i) {
+    if (r < nb) {
+      double v = 0.0;
+      if (r < i) {
+        double s = 0.0;
+        for (int c = r; c < i; ++c) s = fma(sT[r + nb * c], Sp[c + nb * i], s);
+        v = -tp[i] * s;
+      } else if (r == i) {
+        v = tp[i];
+      }
+      sT[r + nb * i] = v;
+    }
+    __syncthreads();
+  }
+  for (int e = r; e < nb * nb; e += blockDim.x) T[(int64_t)p * nb * nb + e] = sT[e];
+}
+
+struct CoopInfo { int blocks = 0; int64_t n = -1; };
+
+}  // namespace
+
+static void orthonormalize(Ctx& c, double* x, int64_t n, int64_t k) {
+  // Newton-Schulz: X <- X (1.5 I - 0.5 X^T X). Converges quadratically from the
+  // eps*||G||/gap non-orthogonality of independently computed eigenvectors.
+  const size_t mk = c.arena.mark();
+  double* w = alloc<double>(c, (size_t)k * k);
+  double* b = alloc<double>(c, (size_t)k * k);
+  double* y = alloc<double>(c, (size_t)n * k);
+  double* chk = alloc<double>(c, 1);
+  auto form_w = [&](const double* xx) {
+    GemmDesc g;
+    g.M = k; g.N = k; g.K1 = n; g.K2 = 1;
+    g.A = xx; g.ta = F64; g.sAm = n; g.sAk1 = 1;     // A(m,kk) = X(kk, m)
+    g.B = xx; g.tb = F64; g.sBn = n; g.sBk1 = 1;     // B(kk,nn) = X(kk, nn)
+    g.C = w; g.sCm = 1; g.sCn = k;
+    g.syrk_upper = true;
+    gemm(c, g);
+    mirror_upper(c, w, k, 1, 0);
+  };
+  form_w(x);
+  maxabs_offidentity(c, w, k, chk);
+  TMB_CUDA(cudaMemcpyAsync(c.host_pinned, chk, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  TMB_CUDA(cudaStreamSynchronize(c.stream));
+  const double e0 = c.host_pinned[0];
+  if (!(e0 < 0.5)) {
+    c.arena.release(mk);
+    throw Error(TMB_ENUMERIC, "leading_eigvecs: eigenvector solve lost orthogonality (clustered eigenvalues); "
+                              "max|X^T X - I| = " + std::to_string(e0));
+  }
+  int iters = e0 < 1e-14 ? 0 : (e0 < 1e-7 ? 1 : (e0 < 1e-3 ? 2 : 4));
+  double* cur = x;
+  double* nxt = y;
+  for (int it = 0; it < iters; ++it) {
+    if (it > 0) form_w(cur);
+    scale_identity_combo(c, w, k, 1.5, -0.5, b);
+    GemmDesc g;
+    g.M = n; g.N = k; g.K1 = k; g.K2 = 1;
+    g.A = cur; g.ta = F64; g.sAm = 1; g.sAk1 = n;
+    g.B = b; g.tb = F64; g.sBn = k; g.sBk1 = 1;
+    g.C = nxt; g.sCm = 1; g.sCn = n;
+    gemm(c, g);
+    std::swap(cur, nxt);
+  }
+  if (cur != x) copy_d(c, x, cur, n * k);
+  c.arena.release(mk);
+}
+
+constexpr int WY_NB = 64;
+
+// x <- H_0 H_1 ... H_{n-3} x by compact-WY panels of WY_NB reflectors, last
+// panel first: x <- x - (V_p T_p) (V_p^T x). hv is n x hv_cols with zero
+// columns past the last reflector; tau is zero-padded likewise.
+static void backtransform(Ctx& c, const double* hv, const double* tau, int64_t n, int64_t hv_cols, int64_t k,
+                          double* x) {
+  const int nb = WY_NB;
+  const int np = (int)(hv_cols / nb);
+  const size_t mk = c.arena.mark();
+  double* S = alloc<double>(c, (size_t)np * nb * nb);
+  double* T = alloc<double>(c, (size_t)np * nb * nb);
+  double* VT = alloc<double>(c, (size_t)np * n * nb);
+  double* W = alloc<double>(c, (size_t)nb * k);
+  {  // S_p = V_p^T V_p for every panel (batched)
+    GemmDesc g;
+    g.M = nb; g.N = nb; g.K1 = n; g.batch = np;
+    g.A = hv; g.sAm = n; g.sAk1 = 1; g.sAb = n * nb;
+    g.B = hv; g.sBn = n; g.sBk1 = 1; g.sBb = n * nb;
+    g.C = S; g.sCm = 1; g.sCn = nb; g.sCb = nb * nb;
+    gemm(c, g);
+  }
+  k_larft<<<np, nb, sizeof(double) * nb * nb, c.stream>>>(S, tau, nb, T);
+  LAUNCHED("k_larft");
+  {  // VT_p = V_p T_p (batched)
+    GemmDesc g;
+    g.M = n; g.N = nb; g.K1 = nb; g.batch = np;
+    g.A = hv; g.sAm = 1; g.sAk1 = n; g.sAb = n * nb;
+    g.B = T; g.sBk1 = 1; g.sBn = nb; g.sBb = nb * nb;
+    g.C = VT; g.sCm = 1; g.sCn = n; g.sCb = n * nb;
+    gemm(c, g);
+  }
+  for (int p = np - 1; p >= 0; --p) {
+    GemmDesc g;  // W = V_p^T x
+    g.M = nb; g.N = k; g.K1 = n;
+    g.A = hv + (int64_t)p * n * nb; g.sAm = n; g.sAk1 = 1;
+    g.B = x; g.sBk1 = 1; g.sBn = n;
+    g.C = W; g.sCm = 1; g.sCn = nb;
+    gemm(c, g);
+    GemmDesc u;  // x -= VT_p W
+    u.M = n; u.N = k; u.K1 = nb;
+    u.A = VT + (int64_t)p * n * nb; u.sAm = 1; u.sAk1 = n;
+    u.B = W; u.sBk1 = 1; u.sBn = nb;
+    u.C = x; u.sCm = 1; u.sCn = n;
+    u.alpha = -1.0; u.beta = 1.0;
+    gemm(c, u);
+  }
+  c.arena.release(mk);
+}
+
+void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs, double* vals) {
+  if (n <= 0 || k <= 0) return;
+  if (n <= JAC_MAX) {
+    const size_t smem = sizeof(double) * 2 * n * (n + 1);
+    static bool attr = false;
+    if (!attr) {
+      TMB_CUDA(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(sizeof(double) * 2 * JAC_MAX * (JAC_MAX + 1))));
+      attr = true;
+    }
+    k_jacobi<<<1, 256, smem, c.stream>>>(g, (int)n, (int)k, vecs, vals);
+    LAUNCHED("k_jacobi");
+    return;
+  }
+  const size_t mk = c.arena.mark();
+  double* A = alloc<double>(c, (size_t)n * n);
+  // Householder vectors: columns 0..n-3 written by k_sytrd, the rest (up to a
+  // whole number of WY panels) stay zero, as do their tau entries.
+  const int64_t hv_cols = ceil_div(n, WY_NB) * WY_NB;
+  double* hv = alloc<double>(c, (size_t)n * hv_cols);
+  double* d = alloc<double>(c, n);
+  double* e = alloc<double>(c, n);
+  double* tau = alloc<double>(c, hv_cols);
+  double* pbuf = alloc<double>(c, 2 * n);
+  TMB_CUDA(cudaMemsetAsync(hv + (n - 2) * n, 0, sizeof(double) * n * (hv_cols - (n - 2)), c.stream));
+  TMB_CUDA(cudaMemsetAsync(tau, 0, sizeof(double) * hv_cols, c.stream));
+  copy_d(c, A, g, n * n);
+  // cooperative grid sized to co-residency
+  const size_t smem = sizeof(double) * (3 * n + 48);
+  static CoopInfo info;
+  if (info.n != n) {
+    TMB_CUDA(cudaFuncSetAttribute(k_sytrd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::max<size_t>(smem, 48 * 1024)));
+    int per_sm = 0;
+    TMB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sytrd, TRD_THREADS, smem));
+    if (per_sm < 1) throw Error(TMB_EINVAL, "leading_eigvecs: matrix too large for the cooperative reduction");
+    // one trailing column per warp when possible
+    info.blocks = (int)std::min<int64_t>((int64_t)per_sm * c.num_sms,
+                                         std::max<int64_t>(1, ceil_div(n, TRD_THREADS / 32)));
+    info.n = n;
+  }
+  const void* kern = (const void*)k_sytrd;
+  const int blocks = info.blocks;
+  double* part = alloc<double>(c, 2 * (size_t)blocks);
+  TrdArgs ta{A, n, d, e, tau, hv, pbuf, part};
+  void* args[] = {&ta};
+  TMB_CUDA(cudaLaunchCooperativeKernel(kern, blocks, TRD_THREADS, args, smem, c.stream));
+  LAUNCHED("k_sytrd");
+  k_bisect<<<(unsigned)ceil_div(k, 8), 256, 0, c.stream>>>(d, e, n, k, vals);
+  LAUNCHED("k_bisect");
+  double* dp = alloc<double>(c, (size_t)n * k);
+  double* dm = alloc<double>(c, (size_t)n * k);
+  double* zrow = alloc<double>(c, (size_t)n * k);
+  k_twisted<<<(unsigned)ceil_div(k, 128), 128, 0, c.stream>>>(d, e, n, k, vals, dp, dm, zrow);
+  LAUNCHED("k_twisted");
+  k_znorm<<<(unsigned)ceil_div(k, 8), 256, 0, c.stream>>>(zrow, n, k, vecs);
+  LAUNCHED("k_znorm");
+  backtransform(c, hv, tau, n, hv_cols, k, vecs);
+  orthonormalize(c, vecs, n, k);
+  sign_fix(c, vecs, n, k);
+  c.arena.release(mk);
+}
+
+}  // namespace tmb

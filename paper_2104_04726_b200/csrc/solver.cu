@@ -1,0 +1,362 @@
+// Host-side Tucker-ALS orchestration over the device kernels (tucker.py).
+// Native C++ runtime: workspace arena, contraction schedule, sweep loop,
+// convergence / best-of bookkeeping. No arithmetic on the host except the
+// control-flow scalars (fit, factor change) read back once per sweep.
+#include "solver.h"
+
+namespace tmb {
+
+// ------------------------------------------------------------------ Arena
+// Stack-disciplined bump allocator over retained cudaMalloc chunks.
+// mark() encodes (chunk index, offset); release() pops back to it.
+Arena::~Arena() { free_all(); }
+
+size_t Arena::capacity() const {
+  size_t s = 0;
+  for (const auto& c : chunks_) s += c.cap;
+  return s;
+}
+
+void* Arena::alloc(size_t bytes) {
+  bytes = std::max<size_t>(256, (bytes + 255) & ~size_t(255));
+  while (cur_ < chunks_.size()) {
+    Chunk& c = chunks_[cur_];
+    if (c.cap - c.used >= bytes) {
+      void* p = c.p + c.used;
+      c.used += bytes;
+      return p;
+    }
+    if (cur_ + 1 < chunks_.size() && chunks_[cur_ + 1].cap >= bytes) { ++cur_; continue; }
+    break;
+  }
+  const size_t cap = std::max<size_t>(bytes, size_t(64) << 20);
+  char* p = nullptr;
+  const cudaError_t e = cudaMalloc(&p, cap);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(TMB_ECUDA, "workspace allocation of " + std::to_string(cap) + " bytes failed: " +
+                               cudaGetErrorString(e));
+  }
+  const size_t pos = chunks_.empty() ? 0 : cur_ + 1;
+  chunks_.insert(chunks_.begin() + pos, Chunk{p, cap, bytes});
+  cur_ = pos;
+  return p;
+}
+
+size_t Arena::mark() const {
+  return chunks_.empty() ? 0 : ((cur_ << 40) | chunks_[cur_].used);
+}
+
+void Arena::release(size_t m) {
+  if (chunks_.empty()) return;
+  const size_t idx = m >> 40, used = m & ((size_t(1) << 40) - 1);
+  cur_ = std::min(idx, chunks_.size() - 1);
+  chunks_[cur_].used = (idx < chunks_.size()) ? used : chunks_[cur_].used;
+  for (size_t j = cur_ + 1; j < chunks_.size(); ++j) chunks_[j].used = 0;
+}
+
+void Arena::free_all() {
+  for (auto& c : chunks_) cudaFree(c.p);
+  chunks_.clear();
+  cur_ = 0;
+}
+
+// ------------------------------------------------------------------ helpers
+int64_t prod(const Dims& d, int a, int b) {
+  int64_t p = 1;
+  for (int i = a; i < b; ++i) p *= d[i];
+  return p;
+}
+
+void ttm_dev(Ctx& c, const void* x, DType tx, const Dims& dims, int mode, const double* m, int64_t r,
+             int64_t sMr, int64_t sMk, double* y) {
+  const int N = (int)dims.size();
+  const int64_t L = prod(dims, 0, mode), K = dims[mode], Rr = prod(dims, mode + 1, N);
+  if (K <= 64 && r <= 64) {
+    small_ttm(c, x, tx, L, K, Rr, m, r, sMr, sMk, y);
+    return;
+  }
+  GemmDesc g;
+  if (L == 1) {  // Y(i, rr) = sum_k M(i,k) X(k, rr): one GEMM over the mode-0 unfolding
+    g.M = r; g.N = Rr; g.K1 = K;
+    g.A = m; g.ta = F64; g.sAm = sMr; g.sAk1 = sMk;
+    g.B = x; g.tb = tx; g.sBk1 = 1; g.sBn = K;
+    g.C = y; g.sCm = 1; g.sCn = r;
+  } else {       // per trailing slab rr: Y_rr(l, i) = sum_k X_rr(l, k) M(i, k)
+    g.M = L; g.N = r; g.K1 = K; g.batch = (int)Rr;
+    g.A = x; g.ta = tx; g.sAm = 1; g.sAk1 = L; g.sAb = L * K;
+    g.B = m; g.tb = F64; g.sBk1 = sMk; g.sBn = sMr;
+    g.C = y; g.sCm = 1; g.sCn = L; g.sCb = L * r;
+  }
+  if (Rr > 32768 && L > 1) {  // grid.z limit: chunk the slabs
+    for (int64_t b0 = 0; b0 < Rr; b0 += 32768) {
+      GemmDesc h = g;
+      h.batch = (int)std::min<int64_t>(32768, Rr - b0);
+      h.A = static_cast<const char*>(x) + b0 * L * K * (tx == F32 ? 4 : 8);
+      h.C = y + b0 * L * r;
+      gemm(c, h);
+    }
+    return;
+  }
+  gemm(c, g);
+}
+
+void mode_gram_dev(Ctx& c, const void* x, DType tx, const Dims& dims, int mode, double* G) {
+  const int N = (int)dims.size();
+  const int64_t L = prod(dims, 0, mode), K = dims[mode], Rr = prod(dims, mode + 1, N);
+  if (K <= 64) {
+    small_gram(c, x, tx, L, K, Rr, G);
+    return;
+  }
+  GemmDesc g;
+  g.M = K; g.N = K;
+  g.A = x; g.ta = tx; g.B = x; g.tb = tx;
+  g.C = G; g.sCm = 1; g.sCn = K;
+  g.syrk_upper = true;
+  if (L == 1) {  // unfolding is the column-major K x Rr matrix itself
+    g.K1 = Rr; g.K2 = 1;
+    g.sAm = 1; g.sAk1 = K;
+    g.sBn = 1; g.sBk1 = K;
+  } else {       // inner index (l, rr): A(i, l, rr) = X[l + L i + L K rr]
+    g.K1 = L; g.K2 = Rr;
+    g.sAm = L; g.sAk1 = 1; g.sAk2 = L * K;
+    g.sBn = L; g.sBk1 = 1; g.sBk2 = L * K;
+  }
+  gemm(c, g);
+  mirror_upper(c, G, K, 1, 0);
+}
+
+// Factor as the TTM matrix: transpose -> M = F^T (F is dims[n] x cols, col-major)
+static void factor_as_m(const double* f, int64_t frows, int64_t fcols, bool transpose, int64_t* r, int64_t* sMr,
+                        int64_t* sMk) {
+  if (transpose) { *r = fcols; *sMr = frows; *sMk = 1; }
+  else { *r = frows; *sMr = 1; *sMk = frows; }
+}
+
+std::vector<int> contraction_order(const Dims& dims, const std::vector<int64_t>& out_rows, int skip, bool greedy) {
+  std::vector<int> modes;
+  for (int n = 0; n < (int)dims.size(); ++n)
+    if (n != skip) modes.push_back(n);
+  if (greedy)  // tensor.py:126-135 (stable sort on out_rows / dim)
+    std::stable_sort(modes.begin(), modes.end(), [&](int a, int b) {
+      return (double)out_rows[a] / (double)dims[a] < (double)out_rows[b] / (double)dims[b];
+    });
+  return modes;
+}
+
+// out = x x_{modes...} factors (ascending or greedy), result written to y.
+void ttmc_dev(Ctx& c, const void* x, DType tx, const Dims& dims, const double* const* factors, const int64_t* frows,
+              const int64_t* fcols, int skip, bool transpose, bool greedy, double* y) {
+  const int N = (int)dims.size();
+  std::vector<int64_t> out_rows(N);
+  for (int n = 0; n < N; ++n) out_rows[n] = transpose ? fcols[n] : frows[n];
+  const std::vector<int> modes = contraction_order(dims, out_rows, skip, greedy);
+  if (modes.empty()) {  // nothing to contract: copy
+    const int64_t P = prod(dims, 0, N);
+    if (tx == F64) copy_d(c, y, static_cast<const double*>(x), P);
+    else convert_f32_f64(c, static_cast<const float*>(x), y, P);
+    return;
+  }
+  const size_t mk = c.arena.mark();
+  Dims cur = dims;
+  const void* src = x;
+  DType st = tx;
+  for (size_t q = 0; q < modes.size(); ++q) {
+    const int n = modes[q];
+    int64_t r, sMr, sMk;
+    factor_as_m(factors[n], frows[n], fcols[n], transpose, &r, &sMr, &sMk);
+    Dims nd = cur;
+    nd[n] = r;
+    double* dst = (q + 1 == modes.size()) ? y : alloc<double>(c, (size_t)prod(nd, 0, N));
+    ttm_dev(c, src, st, cur, n, factors[n], r, sMr, sMk, dst);
+    src = dst;
+    st = F64;
+    cur = nd;
+  }
+  c.arena.release(mk);
+}
+
+// ------------------------------------------------------------------ Tucker steps
+void t_hosvd_dev(Ctx& c, const void* x, DType tx, const Dims& dims, const Dims& ranks, bool greedy, double* core,
+                 double* const* factors) {
+  const int N = (int)dims.size();
+  const size_t mk = c.arena.mark();
+  for (int n = 0; n < N; ++n) {  // tucker.py:141-145
+    double* G = alloc<double>(c, (size_t)dims[n] * dims[n]);
+    double* vals = alloc<double>(c, (size_t)ranks[n]);
+    mode_gram_dev(c, x, tx, dims, n, G);
+    leading_eigvecs(c, G, dims[n], ranks[n], factors[n], vals);
+    c.arena.release(mk);
+  }
+  ttmc_dev(c, x, tx, dims, factors, dims.data(), ranks.data(), -1, true, greedy, core);  // tucker.py:146
+}
+
+// Gauss-Seidel sweep (tucker.py:151-163). Ascending order uses the memoised
+// prefix P_n = t x_0 S_0^T ... x_n S_n^T (updated factors): Y^(n) = P_{n-1}
+// x_{n+1} ... x_{N-1}, the same association order as ttmc(skip=n), with 2 full
+// passes over t per sweep instead of N+1.
+void hooi_sweep_dev(Ctx& c, const void* x, DType tx, const Dims& dims, const Dims& ranks,
+                    const double* const* fin, bool greedy, double* core, double* const* fout) {
+  const int N = (int)dims.size();
+  std::vector<const double*> cur(fin, fin + N);
+  const size_t mk = c.arena.mark();
+  if (greedy) {
+    for (int n = 0; n < N; ++n) {
+      Dims yd = ranks;
+      yd[n] = dims[n];
+      double* Y = alloc<double>(c, (size_t)prod(yd, 0, N));
+      ttmc_dev(c, x, tx, dims, cur.data(), dims.data(), ranks.data(), n, true, true, Y);
+      double* G = alloc<double>(c, (size_t)dims[n] * dims[n]);
+      double* vals = alloc<double>(c, (size_t)ranks[n]);
+      mode_gram_dev(c, Y, F64, yd, n, G);
+      double* nf = (fout[n] == fin[n]) ? alloc<double>(c, (size_t)dims[n] * ranks[n]) : fout[n];
+      leading_eigvecs(c, G, dims[n], ranks[n], nf, vals);
+      if (nf != fout[n]) copy_d(c, fout[n], nf, dims[n] * ranks[n]);
+      cur[n] = fout[n];
+    }
+    ttmc_dev(c, x, tx, dims, cur.data(), dims.data(), ranks.data(), -1, true, true, core);
+    c.arena.release(mk);
+    return;
+  }
+  const void* P = x;  // prefix product with updated factors 0..n-1
+  DType pt = tx;
+  Dims pd = dims;
+  for (int n = 0; n < N; ++n) {
+    // Y^(n) = P x_{n+1} S_{n+1}^T ... x_{N-1} S_{N-1}^T
+    const void* Y = P;
+    DType yt = pt;
+    Dims yd = pd;
+    for (int m = n + 1; m < N; ++m) {
+      Dims nd = yd;
+      nd[m] = ranks[m];
+      double* dst = alloc<double>(c, (size_t)prod(nd, 0, N));
+      ttm_dev(c, Y, yt, yd, m, cur[m], ranks[m], dims[m], 1, dst);
+      Y = dst; yt = F64; yd = nd;
+    }
+    double* G = alloc<double>(c, (size_t)dims[n] * dims[n]);
+    double* vals = alloc<double>(c, (size_t)ranks[n]);
+    mode_gram_dev(c, Y, yt, yd, n, G);
+    double* nf = (fout[n] == fin[n]) ? alloc<double>(c, (size_t)dims[n] * ranks[n]) : fout[n];
+    leading_eigvecs(c, G, dims[n], ranks[n], nf, vals);
+    cur[n] = nf;
+    // P <- P x_n S_n^T
+    Dims nd = pd;
+    nd[n] = ranks[n];
+    double* dst = (n + 1 == N) ? core : alloc<double>(c, (size_t)prod(nd, 0, N));
+    ttm_dev(c, P, pt, pd, n, nf, ranks[n], dims[n], 1, dst);
+    P = dst; pt = F64; pd = nd;
+  }
+  for (int n = 0; n < N; ++n)
+    if (cur[n] != fout[n]) copy_d(c, fout[n], cur[n], dims[n] * ranks[n]);
+  c.arena.release(mk);
+}
+
+void reconstruct_dev(Ctx& c, const Dims& ranks, const Dims& dims, const double* core, const double* const* factors,
+                     double* out) {
+  const int N = (int)dims.size();
+  std::vector<int64_t> frows(dims.begin(), dims.end()), fcols(ranks.begin(), ranks.end());
+  ttmc_dev(c, core, F64, ranks, factors, frows.data(), fcols.data(), -1, false, false, out);  // tucker.py:166-171
+  (void)N;
+}
+
+// ------------------------------------------------------------------ driver
+static double fit_from(double tn, double core_sumsq) {
+  // tucker.py:181-191 with fro_norm = sqrt(sum of squares)
+  const double cn = std::sqrt(core_sumsq);
+  const double resid = std::sqrt(std::max(tn * tn - cn * cn, 0.0));
+  return 1.0 - resid / tn;
+}
+
+void tucker_als_dev(Ctx& c, const void* x, DType tx, const Dims& dims, const Dims& ranks, const tmb_solve_cfg& cfg,
+                    double* core_out, double* const* factors_out, tmb_trace* trace) {
+  const int N = (int)dims.size();
+  const int64_t P = prod(dims, 0, N), Pc = prod(ranks, 0, N);
+  const bool greedy = cfg.sequential_reduction == 0;
+  const double tsq = sumsq(c, x, tx, P);
+  const double tn = std::sqrt(tsq);
+  if (tn == 0.0) throw Error(TMB_EINVAL, "cannot decompose the zero tensor");  // tucker.py:341-342
+  const size_t mk = c.arena.mark();
+  // model buffers: current (a), candidate (b), best
+  auto model_alloc = [&](std::vector<double*>& f) -> double* {
+    f.resize(N);
+    for (int n = 0; n < N; ++n) f[n] = alloc<double>(c, (size_t)dims[n] * ranks[n]);
+    return alloc<double>(c, (size_t)Pc);
+  };
+  std::vector<double*> fa, fb, fbest;
+  double* ca = model_alloc(fa);
+  double* cb = model_alloc(fb);
+  double* cbest = model_alloc(fbest);
+  double* scal = alloc<double>(c, 2 + 2 * N);  // [core sumsq, -, per-mode diff/base pairs]
+  auto rec = [&](int kind, double fit, double change) {
+    if (!trace) return;
+    if (trace->n_records >= trace->capacity) throw Error(TMB_EINVAL, "trace capacity too small");
+    trace->kind[trace->n_records] = kind;
+    trace->fit[trace->n_records] = fit;
+    trace->max_change[trace->n_records] = change;
+    trace->n_records++;
+  };
+  if (trace) { trace->n_records = 0; trace->converged = 0; trace->best_index = 0; }
+
+  t_hosvd_dev(c, x, tx, dims, ranks, greedy, ca, fa.data());  // tucker.py:346
+  sumsq_async(c, ca, F64, Pc, scal);
+  TMB_CUDA(cudaMemcpyAsync(c.host_pinned, scal, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  TMB_CUDA(cudaStreamSynchronize(c.stream));
+  double cur_fit = fit_from(tn, c.host_pinned[0]);
+  rec(TMB_KIND_INIT, cur_fit, std::nan(""));
+  double best_fit = cur_fit;
+  int best_idx = 0;
+  copy_d(c, cbest, ca, Pc);  // tucker.py:349 best = (fit0, init model)
+  for (int n = 0; n < N; ++n) copy_d(c, fbest[n], fa[n], dims[n] * ranks[n]);
+  bool converged = false;
+  if (cur_fit >= 1.0 - cfg.fit_tol) converged = true;  // tucker.py:351-353
+  bool phase_pp = false;
+  double* cc = ca;
+  std::vector<double*>* fc = &fa;
+  double* cn = cb;
+  std::vector<double*>* fn = &fb;
+  for (int sweep = 1; !converged && sweep <= cfg.max_sweeps; ++sweep) {
+    if (phase_pp)
+      throw Error(TMB_ENOTIMPL,
+                  "tucker_als: the solve entered the pairwise-perturbation phase at sweep " + std::to_string(sweep) +
+                      " (max factor change fell below pp_enter_tol); PP sweeps are not implemented on the device "
+                      "path yet -- pass pp_enter_tol=0 to run standard HOOI sweeps");
+    hooi_sweep_dev(c, x, tx, dims, ranks, fc->data(), greedy, cn, fn->data());  // tucker.py:368/373
+    sumsq_async(c, cn, F64, Pc, scal);
+    for (int n = 0; n < N; ++n) diff_norms(c, (*fn)[n], (*fc)[n], dims[n] * ranks[n], scal + 2 + 2 * n);
+    TMB_CUDA(cudaMemcpyAsync(c.host_pinned, scal, sizeof(double) * (2 + 2 * N), cudaMemcpyDeviceToHost, c.stream));
+    TMB_CUDA(cudaStreamSynchronize(c.stream));
+    double change = 0.0;  // tucker.py:319-323
+    for (int n = 0; n < N; ++n)
+      change = std::max(change, std::sqrt(c.host_pinned[2 + 2 * n]) / std::sqrt(c.host_pinned[3 + 2 * n]));
+    const double new_fit = fit_from(tn, c.host_pinned[0]);
+    rec(TMB_KIND_STANDARD, new_fit, change);
+    if (new_fit > best_fit) {  // tucker.py:382-383 (strict)
+      best_fit = new_fit;
+      best_idx = sweep;
+      copy_d(c, cbest, cn, Pc);
+      for (int n = 0; n < N; ++n) copy_d(c, fbest[n], (*fn)[n], dims[n] * ranks[n]);
+    }
+    if (cfg.pp_enter_tol > 0 && change < cfg.pp_enter_tol) phase_pp = true;  // tucker.py:385-387
+    const bool done = std::fabs(new_fit - cur_fit) < cfg.fit_tol;            // tucker.py:389
+    std::swap(cc, cn);
+    std::swap(fc, fn);
+    cur_fit = new_fit;
+    if (done) converged = true;
+  }
+  // tucker.py:395-396: best-fit model when not converged
+  const double* out_core = cc;
+  std::vector<double*>* out_f = fc;
+  int out_idx = trace ? trace->n_records - 1 : 0;
+  if (!converged) {
+    out_idx = best_idx;
+    out_core = cbest;
+    out_f = &fbest;
+  }
+  copy_d(c, core_out, out_core, Pc);
+  for (int n = 0; n < N; ++n) copy_d(c, factors_out[n], (*out_f)[n], dims[n] * ranks[n]);
+  if (trace) { trace->converged = converged ? 1 : 0; trace->best_index = out_idx; }
+  TMB_CUDA(cudaStreamSynchronize(c.stream));
+  c.arena.release(mk);
+}
+
+}  // namespace tmb

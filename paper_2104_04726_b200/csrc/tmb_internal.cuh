@@ -1,0 +1,116 @@
+// Internal declarations shared by the tmb kernels and the host-side solver.
+// Layout conventions: tensors are F-order (mode 0 fastest, the
+// reference's linearisation, tensor.py:1-13); factor matrices are column-major
+// s_n x r_n (one eigenvector per contiguous column); all contraction
+// arithmetic accumulates in fp64.
+#pragma once
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tmb.h"
+
+namespace tmb {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define TMB_CUDA(x)                                                                    \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      throw ::tmb::Error(TMB_ECUDA, std::string(#x ": ") + cudaGetErrorString(e_));    \
+  } while (0)
+
+inline void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(TMB_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Bump arena over retained device chunks: no cudaMalloc inside steady-state loops.
+class Arena {
+ public:
+  ~Arena();
+  void* alloc(size_t bytes);
+  size_t mark() const;
+  void release(size_t mark);
+  void free_all();
+  size_t capacity() const;
+
+ private:
+  struct Chunk { char* p; size_t cap; size_t used; };
+  std::vector<Chunk> chunks_;
+  size_t cur_ = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  std::string err;
+  Arena arena;
+  double* host_pinned = nullptr;   // small D2H staging for scalars
+  int64_t launches = 0;            // kernels launched by this context
+  int coop_blocks = 0;             // resident blocks for cooperative kernels
+};
+
+template <typename T>
+T* alloc(Ctx& c, size_t n) { return static_cast<T*>(c.arena.alloc(n * sizeof(T))); }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------- GEMM (k_gemm.cu)
+enum DType { F32 = 0, F64 = 1 };
+
+// C[b](m,n) = alpha * sum_{k1,k2} A[b](m,k1,k2) B[b](k1,k2,n) + beta * C[b](m,n)
+// with arbitrary element strides; fp64 accumulation on the DMMA pipe.
+struct GemmDesc {
+  int64_t M = 0, N = 0, K1 = 0, K2 = 1;
+  int batch = 1;
+  const void* A = nullptr; DType ta = F64; int64_t sAm = 0, sAk1 = 0, sAk2 = 0, sAb = 0;
+  const void* B = nullptr; DType tb = F64; int64_t sBn = 0, sBk1 = 0, sBk2 = 0, sBb = 0;
+  double* C = nullptr; int64_t sCm = 0, sCn = 0, sCb = 0;
+  double alpha = 1.0, beta = 0.0;
+  bool syrk_upper = false;   // only tiles touching the upper triangle (caller mirrors)
+  int splits = 0;            // 0 = auto
+};
+void gemm(Ctx& c, const GemmDesc& d);
+void mirror_upper(Ctx& c, double* g, int64_t n, int batch, int64_t sb);
+
+// ---------------------------------------------------------------- small kernels (k_small.cu)
+void small_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t Rr,
+               const double* m, int64_t r, int64_t sMr, int64_t sMk, double* y);
+void small_gram(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t Rr, double* g);
+double sumsq(Ctx& c, const void* x, DType tx, int64_t n);           // sync D2H
+void sumsq_async(Ctx& c, const void* x, DType tx, int64_t n, double* out_dev);
+void absmax_async(Ctx& c, const double* x, int64_t n, double* out_dev);
+void quantize(Ctx& c, const double* core, int64_t n, const double* step_dev, int64_t* levels);
+void quant_step(Ctx& c, const double* amax_dev, int qp, double* step_dev);
+void sign_fix(Ctx& c, double* v, int64_t n, int64_t k);
+void diff_norms(Ctx& c, const double* a, const double* b, int64_t n, double* out2_dev);
+void copy_d(Ctx& c, double* dst, const double* src, int64_t n);
+void scale_identity_combo(Ctx& c, const double* w, int64_t n, double a, double b, double* out);
+void maxabs_offidentity(Ctx& c, const double* w, int64_t n, double* out_dev);
+void convert_f32_f64(Ctx& c, const float* s, double* d, int64_t n);
+void dequant(Ctx& c, const int64_t* lv, int64_t n, double step, double* out);
+void axpy(Ctx& c, int64_t n, double alpha, const double* x, double* y);
+void resid2_async(Ctx& c, const void* t, DType tt, const double* that, int64_t n, double* out_dev);
+
+// ---------------------------------------------------------------- eigensolvers (k_eig.cu)
+// Dominant-k eigenpairs of a symmetric n x n (column-major) matrix, eigenvalues
+// nonincreasing, columns sign-fixed (tensor.py:183-209). g is not modified.
+void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs, double* vals);
+
+// ---------------------------------------------------------------- colour (k_color.cu)
+void color_u8(Ctx& c, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, int space, float* out);
+void color_f64(Ctx& c, const double* rgb, int64_t npx, int space, double* out);
+void color_inv_f64(Ctx& c, const double* px, int64_t npx, int space, double* out, int64_t* n_clamped);
+
+}  // namespace tmb

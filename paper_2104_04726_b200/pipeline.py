@@ -1,0 +1,99 @@
+"""The fused hot path: one multi-exposure stereo stack, u8 images -> coding-space
+tensor -> Tucker-ALS -> quantised core (+ reconstruction error), in one
+libtmb call (``tmb_encode_stack_u8``) with every intermediate resident in HBM.
+
+This is the device form of the reference's encode chain for the BASELINE
+configs: ``to_coding_space`` per image (color.py:185-194, codec.py:389) ->
+``tucker_als`` (tucker.py:331-397) -> ``quantize_core`` (codec.py:114-134) ->
+``reconstruct`` (tucker.py:166-171), on the (H, W, 3, V*E) tensor of SURVEY §8.0.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib as L
+from .tensor import DenseTensor
+from .tucker import SolveConfig, SolveTrace, TuckerModel, _trace_buffers, _trace_from_c
+
+__all__ = ["StackResult", "encode_stack", "encode_stack_device", "coding_tensor"]
+
+
+@dataclass
+class StackResult:
+    model: TuckerModel | None
+    trace: SolveTrace
+    levels: np.ndarray | None
+    step: float
+    rel_err: float | None
+    device: dict | None = None  # device tensors when requested
+
+
+def coding_tensor(images_u8, space: str):
+    """(V, E, H, W, 3) uint8 (host ndarray or CUDA tensor) -> float32 CUDA
+    tensor holding the F-order (H, W, 3, V*E) coding-space stack."""
+    torch = L._torch()
+    if isinstance(images_u8, np.ndarray):
+        images_u8 = torch.from_numpy(np.ascontiguousarray(images_u8))
+    if images_u8.dtype != torch.uint8 or images_u8.dim() != 5 or images_u8.shape[-1] != 3:
+        raise ValueError("expected a (V, E, H, W, 3) uint8 image stack")
+    v, e, h, w, _ = images_u8.shape
+    src = images_u8.to("cuda").contiguous()
+    out = torch.empty(h * w * 3 * v * e, dtype=torch.float32, device="cuda")
+    hctx = L.ctx()
+    L.check(L.LIB.tmb_color_u8(hctx, L.ptr(src), v * e, h, w, L.SPACES[space], L.ptr(out)), hctx)
+    return out
+
+
+def encode_stack_device(images_dev, space: str, ranks: Sequence[int], cfg: SolveConfig, qp: int,
+                        rel_err: bool = True, bufs: dict | None = None) -> tuple[dict, L.Trace, float, float | None]:
+    """Device-resident hot path. ``images_dev``: (V, E, H, W, 3) uint8 CUDA
+    tensor. Returns the device buffers dict (tensor, core, factors, levels),
+    the raw trace, the quantiser step and the relative error."""
+    torch = L._torch()
+    v, e, h, w, _ = images_dev.shape
+    dims = (h, w, 3, v * e)
+    ranks = tuple(int(r) for r in ranks)
+    cfg.validate(dims)
+    if bufs is None:
+        bufs = {
+            "tensor": torch.empty(h * w * 3 * v * e, dtype=torch.float32, device="cuda"),
+            "core": L.empty_f64(int(np.prod(ranks))),
+            "factors": [L.empty_f64(s * r) for s, r in zip(dims, ranks)],
+            "levels": torch.empty(int(np.prod(ranks)), dtype=torch.int64, device="cuda"),
+        }
+    tr, _keep = _trace_buffers(cfg.max_sweeps + 1)
+    c = cfg.to_c()
+    step = L.C.c_double()
+    rel = L.C.c_double()
+    hctx = L.ctx()
+    L.check(L.LIB.tmb_encode_stack_u8(hctx, L.ptr(images_dev), v * e, h, w, L.SPACES[space], L.i64s(ranks),
+                                      L.C.byref(c), int(qp), L.ptr(bufs["tensor"]), L.ptr(bufs["core"]),
+                                      L.ptrs(bufs["factors"]), L.ptr(bufs["levels"]), L.C.byref(step),
+                                      L.C.byref(tr), L.C.byref(rel) if rel_err else None), hctx)
+    bufs["_trace_keep"] = _keep
+    return bufs, tr, float(step.value), (float(rel.value) if rel_err else None)
+
+
+def encode_stack(images_u8: np.ndarray, space: str, ranks: Sequence[int], sweeps: int, qp: int,
+                 fit_tol: float = 1e-300, pp_enter_tol: float = 0.0, rel_err: bool = True,
+                 return_model: bool = True) -> StackResult:
+    """Host API for one stack: H2D of the u8 images, the fused device path,
+    D2H of the quantised levels (and optionally the model)."""
+    torch = L._torch()
+    imgs = torch.from_numpy(np.ascontiguousarray(images_u8)).to("cuda")
+    v, e, h, w, _ = imgs.shape
+    dims = (h, w, 3, v * e)
+    cfg = SolveConfig(ranks=tuple(ranks), max_sweeps=sweeps, fit_tol=fit_tol, pp_enter_tol=pp_enter_tol)
+    bufs, tr, step, rel = encode_stack_device(imgs, space, ranks, cfg, qp, rel_err=rel_err)
+    ranks = tuple(int(r) for r in ranks)
+    levels = np.reshape(bufs["levels"][: int(np.prod(ranks))].cpu().numpy(), ranks, order="F")
+    model = None
+    if return_model:
+        core = DenseTensor(L.host_f(bufs["core"], ranks))
+        facs = [L.host_f(f, (dims[n], ranks[n])) for n, f in enumerate(bufs["factors"])]
+        model = TuckerModel(core, facs, dims)
+    return StackResult(model, _trace_from_c(tr), levels, step, rel, bufs)

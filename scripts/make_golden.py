@@ -1,0 +1,146 @@
+"""Generate tests/golden/*.npz by running the REFERENCE implementation itself.
+
+Run in the build container only (it imports /root/reference/pkg/src):
+
+    PYTHONDONTWRITEBYTECODE=1 OPENBLAS_NUM_THREADS=8 python scripts/make_golden.py
+
+The fixtures pin both the CPU oracle (oracle/) and the CUDA path. Each case
+stores the synthetic uint8 input stack, the solve configuration, and the
+reference's factors, core, trace, quantised levels/step and relative error.
+Inputs follow SURVEY.md Appendix B 1(i): the reference colour transform in
+float64, rounded to float32 (the device tensor format), upcast to float64 and
+handed to ``tucker_als`` with ``SolveConfig(max_sweeps=K, fit_tol=1e-300,
+pp_enter_tol=0.0)`` for exactly K sweeps.
+"""
+
+from __future__ import annotations
+
+import os
+import platform
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, REF)
+sys.path.insert(0, str(ROOT))
+
+from tmcodec.codec import quantize_core  # noqa: E402
+from tmcodec.color import ColorImage, to_coding_space  # noqa: E402
+from tmcodec.tensor import DenseTensor  # noqa: E402
+from tmcodec.tucker import SolveConfig, reconstruct, tucker_als  # noqa: E402
+
+from paper_2104_04726_b200.synth import CONFIGS, make_stack, qp_for_bits  # noqa: E402
+
+OUT = ROOT / "tests" / "golden"
+
+# name -> (base config, seed, height, width, ranks, sweeps, bits)
+CASES = {
+    "c1": ("c1", 0, 384, 512, (48, 64, 3, 3), 10, 8),
+    "c2q": ("c2", 1, 270, 480, (68, 120, 3, 5), 20, 10),
+    "c3q": ("c3", 2, 270, 480, (34, 60, 3, 5), 10, 8),
+}
+
+
+def ref_tensor(images: np.ndarray, space: str) -> np.ndarray:
+    v_, e_, h, w, _ = images.shape
+    t = np.empty((h, w, 3, v_ * e_), order="F")
+    for v in range(v_):
+        for e in range(e_):
+            img = ColorImage(images[v, e].astype(np.float64) / 255.0)
+            t[:, :, :, v * e_ + e] = to_coding_space(img, space).pixels
+    return t
+
+
+def run_case(name: str) -> None:
+    base, seed, h, w, ranks, sweeps, bits = CASES[name]
+    cfg = CONFIGS[base]
+    images = make_stack(cfg, seed=seed, height=h, width=w)
+    t64 = ref_tensor(images, cfg.space)
+    t32 = t64.astype(np.float32)
+    x = np.asfortranarray(t32.astype(np.float64))
+    t0 = time.time()
+    model, trace = tucker_als(
+        DenseTensor(x), SolveConfig(ranks=ranks, max_sweeps=sweeps, fit_tol=1e-300, pp_enter_tol=0.0)
+    )
+    dt = time.time() - t0
+    q = quantize_core(model, qp_for_bits(bits))
+    rec = reconstruct(model).array
+    rel = float(np.linalg.norm((x - rec).ravel()) / np.linalg.norm(x.ravel()))
+    rows = trace.rows()
+    sample = np.random.default_rng(123).integers(0, x.size, 4096)
+    np.savez_compressed(
+        OUT / f"{name}.npz",
+        images=images,
+        space=np.array(cfg.space),
+        ranks=np.array(ranks),
+        sweeps=np.array(sweeps),
+        qp=np.array(qp_for_bits(bits)),
+        tensor_sample_idx=sample,
+        tensor_sample_f64=t64.ravel(order="F")[sample],
+        tensor_f32_sha=np.array(__import__("hashlib").sha256(np.asfortranarray(t32).tobytes(order="F")).hexdigest()),
+        core=model.core.array,
+        **{f"factor{n}": f for n, f in enumerate(model.factors)},
+        levels=q.levels,
+        step=np.array(q.step),
+        trace_fit=np.array([r[2] for r in rows]),
+        trace_change=np.array([r[3] for r in rows]),
+        trace_kind=np.array([r[1] for r in rows]),
+        converged=np.array(trace.converged),
+        rel_err=np.array(rel),
+        env=np.array(f"numpy {np.__version__}; OPENBLAS_NUM_THREADS={os.environ.get('OPENBLAS_NUM_THREADS')}; "
+                     f"{platform.processor() or platform.machine()}; solve {dt:.2f}s"),
+    )
+    print(name, "fit", rows[-1][2], "rel", rel, f"{dt:.1f}s")
+
+
+def colour_kat() -> None:
+    """Reference colour transforms on every gray level and 2000 random u8 triples."""
+    rng = np.random.default_rng(5)
+    g = np.arange(256, dtype=np.float64)[:, None].repeat(3, axis=1)
+    rnd = rng.integers(0, 256, size=(2000, 3)).astype(np.float64)
+    u8 = np.concatenate([g, rnd]).astype(np.uint8)
+    px = (u8.astype(np.float64) / 255.0)[None]
+    fpx = rng.uniform(0.0, 1.0, size=(1, 500, 3))
+    out = {"u8": u8, "fpx": fpx}
+    for space in ("ycbcr", "ipt"):
+        out[f"{space}_u8"] = to_coding_space(ColorImage(px), space).pixels[0]
+        out[f"{space}_f"] = to_coding_space(ColorImage(fpx), space).pixels[0]
+    np.savez_compressed(OUT / "colour.npz", **out)
+    print("colour KAT written")
+
+
+def api_cases() -> None:
+    """Small f64 solves with the reference defaults (PP-capable config) and
+    exact-K solves, for drop-in API parity at fp64 tolerances."""
+    rng = np.random.default_rng(11)
+    out = {}
+    specs = [((6, 7, 5), (3, 4, 2), 8), ((9, 8, 4, 3), (4, 3, 2, 2), 6), ((12, 10), (3, 3), 5)]
+    for k, (dims, ranks, sweeps) in enumerate(specs):
+        x = rng.standard_normal(dims)
+        model, trace = tucker_als(DenseTensor(x), SolveConfig(ranks=ranks, max_sweeps=sweeps,
+                                                               fit_tol=1e-300, pp_enter_tol=0.0))
+        out[f"x{k}"] = x
+        out[f"ranks{k}"] = np.array(ranks)
+        out[f"sweeps{k}"] = np.array(sweeps)
+        out[f"core{k}"] = model.core.array
+        for n, f in enumerate(model.factors):
+            out[f"f{k}_{n}"] = f
+        out[f"fit{k}"] = np.array([r[2] for r in trace.rows()])
+    np.savez_compressed(OUT / "api.npz", **out)
+    print("api cases written")
+
+
+if __name__ == "__main__":
+    OUT.mkdir(parents=True, exist_ok=True)
+    names = sys.argv[1:] or (list(CASES) + ["colour", "api"])
+    for nm in names:
+        if nm == "colour":
+            colour_kat()
+        elif nm == "api":
+            api_cases()
+        else:
+            run_case(nm)

@@ -102,6 +102,17 @@ const char* tmb_last_error(const tmb_ctx* ctx) { return ctx ? ctx->c.err.c_str()
 
 int64_t tmb_launch_count(const tmb_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
 
+int tmb_timing(tmb_ctx* ctx, int enable) {
+  return guard(ctx, [&](tmb::Ctx& c) { tmb::timing_enable(c, enable != 0); });
+}
+
+int tmb_timing_read(tmb_ctx* ctx, int tag, int64_t* count, double* ms, double* work) {
+  return guard(ctx, [&](tmb::Ctx& c) {
+    if (tag < 0 || tag >= tmb::TAG_COUNT) throw Error(TMB_EINVAL, "unknown timer tag");
+    tmb::timing_read(c, tag, count, ms, work);
+  });
+}
+
 int tmb_color_u8(tmb_ctx* ctx, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, int space, float* out) {
   return guard(ctx, [&](tmb::Ctx& c) {
     if (space < TMB_SPACE_RGB || space > TMB_SPACE_IPT) throw Error(TMB_EINVAL, "unknown color space");

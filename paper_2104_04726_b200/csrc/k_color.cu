@@ -211,6 +211,7 @@ void color_u8(Ctx& c, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, i
   if (n_img == 0 || h == 0 || w == 0) return;
   ensure_constants(c);
   dim3 grid((unsigned)ceil_div(w, 32), (unsigned)ceil_div(h, 32), (unsigned)n_img);
+  Timed timed(c, TAG_COLOR, 15.0 * (double)n_img * h * w);  // 3 B read + 12 B written per pixel
   k_color_u8<<<grid, dim3(32, 8), 0, c.stream>>>(rgb, h, w, space, out);
   c.launches++;
   check_launch("k_color_u8");

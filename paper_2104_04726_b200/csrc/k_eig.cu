@@ -699,17 +699,23 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
   double* part = alloc<double>(c, 2 * (size_t)blocks);
   TrdArgs ta{A, n, d, e, tau, hv, pbuf, part};
   void* args[] = {&ta};
-  TMB_CUDA(cudaLaunchCooperativeKernel(kern, blocks, TRD_THREADS, args, smem, c.stream));
-  LAUNCHED("k_sytrd");
-  k_bisect<<<(unsigned)ceil_div(k, 8), 256, 0, c.stream>>>(d, e, n, k, vals);
-  LAUNCHED("k_bisect");
+  {
+    Timed timed(c, TAG_SYTRD, 4.0 / 3.0 * (double)n * n * n);  // dsytrd flop count
+    TMB_CUDA(cudaLaunchCooperativeKernel(kern, blocks, TRD_THREADS, args, smem, c.stream));
+    LAUNCHED("k_sytrd");
+  }
   double* dp = alloc<double>(c, (size_t)n * k);
   double* dm = alloc<double>(c, (size_t)n * k);
   double* zrow = alloc<double>(c, (size_t)n * k);
-  k_twisted<<<(unsigned)ceil_div(k, 128), 128, 0, c.stream>>>(d, e, n, k, vals, dp, dm, zrow);
-  LAUNCHED("k_twisted");
-  k_znorm<<<(unsigned)ceil_div(k, 8), 256, 0, c.stream>>>(zrow, n, k, vecs);
-  LAUNCHED("k_znorm");
+  {
+    Timed timed_tri(c, TAG_TRIDIAG, 0.0);
+    k_bisect<<<(unsigned)ceil_div(k, 8), 256, 0, c.stream>>>(d, e, n, k, vals);
+    LAUNCHED("k_bisect");
+    k_twisted<<<(unsigned)ceil_div(k, 128), 128, 0, c.stream>>>(d, e, n, k, vals, dp, dm, zrow);
+    LAUNCHED("k_twisted");
+    k_znorm<<<(unsigned)ceil_div(k, 8), 256, 0, c.stream>>>(zrow, n, k, vecs);
+    LAUNCHED("k_znorm");
+  }
   backtransform(c, hv, tau, n, hv_cols, k, vecs);
   orthonormalize(c, vecs, n, k);
   sign_fix(c, vecs, n, k);

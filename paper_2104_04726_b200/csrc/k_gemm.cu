@@ -248,6 +248,10 @@ void gemm(Ctx& c, const GemmDesc& d0) {
   if (splits > 1) a.part = alloc<double>(c, (size_t)splits * d.batch * d.M * d.N);
   if (tm > 65535) throw Error(TMB_EINVAL, "gemm: M too large for the tile grid");
   dim3 grid((unsigned)tn, (unsigned)tm, (unsigned)(d.batch * splits));
+  // algorithmic flops: 2mnk per product, s(s+1)K for a SYRK
+  const double kk = (double)d.K1 * (double)d.K2 * d.batch;
+  const double work = d.syrk_upper ? (double)d.M * (d.M + 1) * kk : 2.0 * d.M * d.N * kk;
+  Timed timed(c, TAG_GEMM, work);
   if (d.ta == F64 && d.tb == F64) launch_t<double, double>(c, a, grid);
   else if (d.ta == F32 && d.tb == F64) launch_t<float, double>(c, a, grid);
   else if (d.ta == F64 && d.tb == F32) launch_t<double, float>(c, a, grid);

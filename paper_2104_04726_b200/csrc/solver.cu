@@ -61,6 +61,52 @@ void Arena::free_all() {
   cur_ = 0;
 }
 
+// ------------------------------------------------------------------ kernel timer
+static cudaEvent_t take_event(Ctx& c) {
+  KernelTimes& k = c.kt;
+  if (k.used == k.pool.size()) {
+    cudaEvent_t e;
+    TMB_CUDA(cudaEventCreate(&e));
+    k.pool.push_back(e);
+  }
+  return k.pool[k.used++];
+}
+
+Timed::Timed(Ctx& c, int tag, double work) : c_(c), tag_(tag), work_(work) {
+  if (!c_.timing) return;
+  a_ = c_.kt.used;
+  TMB_CUDA(cudaEventRecord(take_event(c_), c_.stream));
+}
+
+Timed::~Timed() {
+  if (!c_.timing) return;
+  const size_t b = c_.kt.used;
+  if (cudaEventRecord(take_event(c_), c_.stream) == cudaSuccess) c_.kt.recs.push_back({tag_, a_, b, work_});
+}
+
+void timing_enable(Ctx& c, bool on) {
+  c.timing = on;
+  c.kt.used = 0;
+  c.kt.recs.clear();
+}
+
+void timing_read(Ctx& c, int tag, int64_t* count, double* ms, double* work) {
+  TMB_CUDA(cudaStreamSynchronize(c.stream));
+  int64_t n = 0;
+  double t = 0.0, w = 0.0;
+  for (const auto& r : c.kt.recs) {
+    if (r.tag != tag) continue;
+    float e = 0.f;
+    TMB_CUDA(cudaEventElapsedTime(&e, c.kt.pool[r.a], c.kt.pool[r.b]));
+    ++n;
+    t += e;
+    w += r.work;
+  }
+  *count = n;
+  *ms = t;
+  *work = w;
+}
+
 // ------------------------------------------------------------------ helpers
 int64_t prod(const Dims& d, int a, int b) {
   int64_t p = 1;

@@ -7,6 +7,8 @@ namespace tmb {
 using Dims = std::vector<int64_t>;
 
 int64_t prod(const Dims& d, int a, int b);
+void timing_enable(Ctx& c, bool on);
+void timing_read(Ctx& c, int tag, int64_t* count, double* ms, double* work);
 void ttm_dev(Ctx& c, const void* x, DType tx, const Dims& dims, int mode, const double* m, int64_t r,
              int64_t sMr, int64_t sMk, double* y);
 void mode_gram_dev(Ctx& c, const void* x, DType tx, const Dims& dims, int mode, double* G);

@@ -50,6 +50,16 @@ class Arena {
   size_t cur_ = 0;
 };
 
+// Per-family launch timing (CUDA events on the context stream), enabled by the
+// benchmark to measure the dominant kernel's live launch durations.
+struct KernelTimes {
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  struct Rec { int tag; size_t a, b; double work; };
+  std::vector<Rec> recs;
+};
+enum TimerTag { TAG_GEMM = 0, TAG_SYTRD, TAG_TRIDIAG, TAG_COLOR, TAG_SMALL, TAG_COUNT };
+
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -59,6 +69,22 @@ struct Ctx {
   double* host_pinned = nullptr;   // small D2H staging for scalars
   int64_t launches = 0;            // kernels launched by this context
   int coop_blocks = 0;             // resident blocks for cooperative kernels
+  bool timing = false;
+  KernelTimes kt;
+  double work[TAG_COUNT] = {0};    // algorithmic flops/bytes attributed per tag
+};
+
+// RAII: records an event pair around the launches in its scope (if enabled)
+// and attributes `work` algorithmic units (flops or bytes) to the tag.
+class Timed {
+ public:
+  Timed(Ctx& c, int tag, double work);
+  ~Timed();
+ private:
+  Ctx& c_;
+  int tag_;
+  size_t a_ = 0;
+  double work_;
 };
 
 template <typename T>

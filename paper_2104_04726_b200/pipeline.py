@@ -84,7 +84,9 @@ def encode_stack(images_u8: np.ndarray, space: str, ranks: Sequence[int], sweeps
     """Host API for one stack: H2D of the u8 images, the fused device path,
     D2H of the quantised levels (and optionally the model)."""
     torch = L._torch()
-    imgs = torch.from_numpy(np.ascontiguousarray(images_u8)).to("cuda")
+    if isinstance(images_u8, np.ndarray):
+        images_u8 = torch.from_numpy(np.ascontiguousarray(images_u8))
+    imgs = images_u8.to("cuda", non_blocking=True)  # async from pinned host memory
     v, e, h, w, _ = imgs.shape
     dims = (h, w, 3, v * e)
     cfg = SolveConfig(ranks=tuple(ranks), max_sweeps=sweeps, fit_tol=fit_tol, pp_enter_tol=pp_enter_tol)

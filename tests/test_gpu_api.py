@@ -1,0 +1,368 @@
+"""Drop-in API contract tests on the device path (ports of the reference's
+tests/test_tensor.py, test_tucker.py, test_pp.py, test_color.py and
+test_codec.py at the reference's own fp64 tolerances), plus oracle
+comparisons for every kernel family. Every call goes through libtmb."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2104_04726_b200 as tb
+from paper_2104_04726_b200 import _lib as L
+
+pytestmark = pytest.mark.gpu
+
+
+def rand_orth(rng, rows, cols):
+    return np.linalg.qr(rng.standard_normal((rows, cols)))[0]
+
+
+def random_tucker_tensor(rng, dims, ranks):
+    core = tb.DenseTensor(rng.standard_normal(ranks))
+    model = tb.TuckerModel(core, [rand_orth(rng, s, r) for s, r in zip(dims, ranks)], tuple(dims))
+    return tb.reconstruct(model), model
+
+
+def rel_err(a, b):
+    return float(np.linalg.norm(a.array - b.array) / np.linalg.norm(a.array))
+
+
+# ------------------------------------------------------------------ tensor.py
+def test_ttm_identity_and_oracle():
+    rng = np.random.default_rng(1)
+    t = tb.DenseTensor(rng.standard_normal((4, 3, 5)))
+    for n in range(3):
+        assert np.abs(tb.ttm(t, np.eye(t.dims[n]), n).array - t.array).max() < 1e-15
+        m = rng.standard_normal((6, t.dims[n]))
+        assert np.abs(tb.ttm(t, m, n).array - oracle.ttm(t.array, m, n)).max() < 1e-12
+
+
+def test_ttm_large_modes_gemm_path():
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((130, 97, 4, 3))
+    for n, r in [(0, 70), (1, 80)]:
+        m = rng.standard_normal((r, x.shape[n]))
+        got = tb.ttm(tb.DenseTensor(x), m, n).array
+        ref = oracle.ttm(x, m, n)
+        assert np.abs(got - ref).max() / np.abs(ref).max() < 1e-13
+
+
+def test_ttmc_nested_loop_oracle_and_orders():  # tests/test_tensor.py:127-165
+    rng = np.random.default_rng(4)
+    t = tb.DenseTensor(rng.standard_normal((3, 3, 3)))
+    fs = [rng.standard_normal((3, 2)) for _ in range(3)]
+    out = tb.ttmc(t, fs).array
+    expect = np.einsum("abc,ai,bj,ck->ijk", t.array, *fs)
+    assert np.abs(out - expect).max() < 1e-12
+    t4 = tb.DenseTensor(rng.standard_normal((6, 5, 4, 3)))
+    f4 = [rand_orth(rng, s, 2) for s in t4.dims]
+    a = tb.ttmc(t4, f4, order="ascending").array
+    g = tb.ttmc(t4, f4, order="greedy").array
+    assert np.abs(a - g).max() < 1e-12
+
+
+def test_ttmc_skip_hand_case():  # tests/test_tensor.py:149-156
+    t = tb.DenseTensor.from_flat(np.arange(1.0, 9.0), (2, 2, 2))
+    u = np.array([[1.0], [1.0]])
+    out = tb.ttmc(t, [None, u, u], skip=0)
+    assert out.dims == (2, 1, 1)
+    assert np.allclose(out.array[:, 0, 0], [16.0, 20.0])
+
+
+def test_ttmc_error_names_mode():  # tests/test_tensor.py:167-172
+    t = tb.DenseTensor(np.ones((2, 3, 4)))
+    with pytest.raises(ValueError, match="mode 1"):
+        tb.ttmc(t, [np.eye(2), np.eye(2), np.eye(4)])
+
+
+def test_gram_exact_symmetry_and_oracle():  # tests/test_tensor.py:184-194
+    rng = np.random.default_rng(5)
+    for shape in [(5, 9), (120, 300), (70, 40)]:
+        m = rng.standard_normal(shape)
+        g = tb.gram(m)
+        assert np.array_equal(g, g.T)
+        ref = oracle.gram(m)
+        assert np.abs(g - ref).max() / np.abs(ref).max() < 1e-14
+
+
+def test_mode_gram_matches_unfold_gram():
+    rng = np.random.default_rng(6)
+    x = rng.standard_normal((80, 70, 3, 5))
+    for n in range(4):
+        got = tb.mode_gram(tb.DenseTensor(x), n)
+        ref = oracle.gram(oracle.unfold(x, n))
+        assert np.abs(got - ref).max() / np.abs(ref).max() < 1e-13
+
+
+def test_eig_diagonal_and_sign_rule():  # tests/test_tensor.py:196-207
+    v, w = tb.leading_eigvecs(np.diag([3.0, 2.0, 1.0]), 2)
+    assert np.allclose(w, [3, 2]) and np.allclose(v, [[1, 0], [0, 1], [0, 0]])
+    v1, _ = tb.leading_eigvecs(np.outer([0.6, -0.8], [0.6, -0.8]), 1)
+    assert np.allclose(v1[:, 0], [-0.6, 0.8])
+
+
+@pytest.mark.parametrize("n,k", [(7, 7), (33, 10), (64, 64), (65, 20), (200, 50), (700, 100)])
+def test_eig_residual_orthonormal_vs_lapack(n, k):  # tests/test_tensor.py:209-216
+    rng = np.random.default_rng(n)
+    b = rng.standard_normal((n, n))
+    g = b @ b.T
+    v, w = tb.leading_eigvecs(g, k)
+    vr, wr = oracle.leading_eigvecs(g, k)
+    assert np.abs(v.T @ v - np.eye(k)).max() < 1e-10
+    assert np.abs(g @ v - v * w).max() / wr[0] < 1e-10
+    assert np.abs(w - wr).max() / wr[0] < 1e-12
+    assert np.abs(v - vr).max() < 1e-7            # same columns, same signs (sign rule)
+
+
+def test_eig_graded_spectrum_large():
+    """Image-like Gram: eigenvalues over 1e8, tridiagonal path."""
+    rng = np.random.default_rng(8)
+    n, k = 1080, 270
+    q = rand_orth(rng, n, n)
+    lam = 1e3 * np.exp(-np.linspace(0, 20, n))
+    g = (q * lam) @ q.T
+    g = 0.5 * (g + g.T)
+    v, w = tb.leading_eigvecs(g, k)
+    vr, wr = oracle.leading_eigvecs(g, k)
+    from conftest import principal_angle
+
+    assert principal_angle(v, vr) < 1e-9
+    assert np.abs(v.T @ v - np.eye(k)).max() < 1e-12
+    assert np.abs(w - wr).max() / wr[0] < 1e-13
+
+
+def test_eig_deterministic():  # tests/test_tensor.py:218-223
+    rng = np.random.default_rng(9)
+    b = rng.standard_normal((300, 300))
+    g = b @ b.T
+    a1, w1 = tb.leading_eigvecs(g, 40)
+    a2, w2 = tb.leading_eigvecs(g, 40)
+    assert np.array_equal(a1, a2) and np.array_equal(w1, w2)
+
+
+def test_fro_norm():  # tests/test_tensor.py:232-242
+    assert tb.fro_norm(tb.DenseTensor(np.zeros((2, 2)))) == 0.0
+    assert tb.fro_norm(tb.DenseTensor(np.ones((2, 3, 4)))) == pytest.approx(np.sqrt(24.0), rel=1e-15)
+
+
+# ------------------------------------------------------------------ tucker.py
+def test_hosvd_single_nonzero():  # tests/test_tucker.py:37-48
+    arr = np.zeros((3, 3, 3))
+    arr[1, 2, 0] = 5.0
+    model = tb.hosvd(tb.DenseTensor(arr))
+    mags = np.sort(np.abs(model.core.array).ravel())
+    assert mags[-1] == pytest.approx(5.0) and mags[-2] < 1e-12
+    for f in model.factors:
+        assert np.allclose(np.abs(f).sum(axis=0), 1.0) and np.allclose(np.abs(f).max(axis=0), 1.0)
+
+
+def test_hosvd_reconstruction_and_svd():  # tests/test_tucker.py:50-68
+    rng = np.random.default_rng(0)
+    t = tb.DenseTensor(rng.standard_normal((4, 4, 4)))
+    model = tb.hosvd(t)
+    model.validate()
+    assert rel_err(t, tb.reconstruct(model)) < 1e-10
+    a = np.random.default_rng(1).standard_normal((5, 7))
+    u = tb.hosvd(tb.DenseTensor(a)).factors[0]
+    u_svd = np.linalg.svd(a)[0]
+    for j in range(5):
+        col = u_svd[:, j]
+        col = -col if col[np.argmax(np.abs(col))] < 0 else col
+        assert np.allclose(u[:, j], col, atol=1e-8)
+
+
+def test_thosvd_full_equals_hosvd_and_exact_recovery():  # tests/test_tucker.py:72-86
+    rng = np.random.default_rng(2)
+    t = tb.DenseTensor(rng.standard_normal((3, 4, 5)))
+    a, b = tb.hosvd(t), tb.t_hosvd(t, (3, 4, 5))
+    for fa, fb in zip(a.factors, b.factors):
+        assert np.array_equal(fa, fb)
+    assert np.array_equal(a.core.array, b.core.array)
+    t2, _ = random_tucker_tensor(np.random.default_rng(3), (6, 6, 6), (2, 2, 2))
+    m = tb.t_hosvd(t2, (2, 2, 2))
+    m.validate()
+    assert rel_err(t2, tb.reconstruct(m)) < 1e-8
+
+
+def test_thosvd_error_bound():  # tests/test_tucker.py:88-100
+    for seed in range(3):
+        rng = np.random.default_rng(seed)
+        t = tb.DenseTensor(rng.standard_normal((6, 5, 4)))
+        model = tb.t_hosvd(t, (2, 2, 2))
+        err2 = float(np.linalg.norm(t.array - tb.reconstruct(model).array) ** 2)
+        bound = sum(float(np.sum(np.sort(np.linalg.eigvalsh(oracle.gram(oracle.unfold(t.array, n))))[::-1][2:]))
+                    for n in range(3))
+        assert err2 <= bound * (1 + 1e-8) + 1e-10
+
+
+def test_hooi_fixed_point_and_monotone():  # tests/test_tucker.py:130-147
+    rng = np.random.default_rng(7)
+    t, _ = random_tucker_tensor(rng, (6, 5, 4), (2, 2, 2))
+    start = tb.t_hosvd(t, (2, 2, 2))
+    swept = tb.hooi_sweep(t, start)
+    for a, b in zip(swept.factors, start.factors):
+        assert np.allclose(a, b, atol=1e-8)
+    assert tb.fit(t, swept) >= 1 - 1e-7
+    t3 = tb.DenseTensor(np.random.default_rng(8).standard_normal((5, 5, 5)))
+    m = tb.t_hosvd(t3, (2, 2, 2))
+    assert tb.fit(t3, tb.hooi_sweep(t3, m)) >= tb.fit(t3, m) - 1e-12
+
+
+def test_hooi_matches_oracle_sweep():
+    rng = np.random.default_rng(10)
+    x = rng.standard_normal((9, 8, 4, 3))
+    ranks = (4, 3, 2, 2)
+    m0 = tb.t_hosvd(tb.DenseTensor(x), ranks)
+    core_o, fac_o = oracle.t_hosvd(x, ranks)
+    for a, b in zip(m0.factors, fac_o):
+        assert np.abs(a - b).max() < 1e-10
+    m1 = tb.hooi_sweep(tb.DenseTensor(x), m0)
+    core1, fac1 = oracle.hooi_sweep(x, fac_o)
+    for a, b in zip(m1.factors, fac1):
+        assert np.abs(a - b).max() < 1e-9
+    assert np.abs(m1.core.array - core1).max() < 1e-10
+
+
+def test_fit_and_reconstruct_contracts():  # tests/test_tucker.py:169-254
+    rng = np.random.default_rng(11)
+    t = tb.DenseTensor(rng.standard_normal((6, 5, 4)))
+    model = tb.t_hosvd(t, (3, 3, 2))
+    assert abs(tb.fit(t, model) - tb.fit(t, model, method="residual")) < 1e-10
+    with pytest.raises(ValueError):
+        tb.fit(tb.DenseTensor(np.zeros((2, 2))), model)
+    core = rng.standard_normal((2, 3, 2))
+    fs = [rng.standard_normal((4, 2)), rng.standard_normal((3, 3)), rng.standard_normal((5, 2))]
+    got = tb.reconstruct(tb.TuckerModel(tb.DenseTensor(core), fs, (4, 3, 5))).array
+    expect = np.einsum("abc,ia,jb,kc->ijk", core, *fs)
+    assert np.abs(got - expect).max() < 1e-12
+
+
+def test_tucker_als_contracts():  # tests/test_tucker.py:258-313
+    rng = np.random.default_rng(18)
+    t, _ = random_tucker_tensor(rng, (8, 9, 8), (2, 3, 2))
+    model, trace = tb.tucker_als(t, tb.SolveConfig(ranks=(2, 3, 2), max_sweeps=10))
+    assert trace.converged and tb.fit(t, model) >= 1 - 1e-6
+    model.validate()
+    t2 = tb.DenseTensor(np.random.default_rng(19).standard_normal((4, 5, 3)))
+    model2, trace2 = tb.tucker_als(t2, tb.SolveConfig(ranks=(4, 5, 3)))
+    assert trace2.converged and len(trace2.records) == 1 and trace2.records[0].kind == "init"
+    t3 = tb.DenseTensor(np.random.default_rng(20).standard_normal((16, 16, 10)))
+    _, tr3 = tb.tucker_als(t3, tb.SolveConfig(ranks=(4, 4, 3), max_sweeps=20, fit_tol=1e-9, pp_enter_tol=0.0))
+    fits = [r.fit for r in tr3.records]
+    assert all(r.kind in ("init", "standard") for r in tr3.records)
+    assert all(b >= a - 1e-12 for a, b in zip(fits, fits[1:]))
+    with pytest.raises(ValueError):
+        tb.tucker_als(tb.DenseTensor(np.zeros((3, 3))), tb.SolveConfig(ranks=(2, 2)))
+    t4 = tb.DenseTensor(np.random.default_rng(21).standard_normal((10, 10, 10)))
+    m4, tr4 = tb.tucker_als(t4, tb.SolveConfig(ranks=(3, 3, 3), max_sweeps=1, fit_tol=1e-14, pp_enter_tol=0.0))
+    assert not tr4.converged
+    m4.validate()
+
+
+def test_tucker_als_greedy_matches_sequential():  # tests/test_tucker.py:315-321 (PP off)
+    t = tb.DenseTensor(np.random.default_rng(23).standard_normal((9, 7, 5, 3)))
+    ranks = (3, 3, 2, 2)
+    kw = dict(ranks=ranks, pp_enter_tol=0.0, max_sweeps=30)
+    f_seq = tb.fit(t, tb.tucker_als(t, tb.SolveConfig(sequential_reduction=True, **kw))[0])
+    f_gr = tb.fit(t, tb.tucker_als(t, tb.SolveConfig(sequential_reduction=False, **kw))[0])
+    assert abs(f_seq - f_gr) < 1e-9
+
+
+def test_api_goldens_reference_parity(golden):
+    """Reference tucker_als on random f64 tensors (tests/golden/api.npz)."""
+    z = golden("api")
+    for k in range(3):
+        t = tb.DenseTensor(z[f"x{k}"])
+        cfg = tb.SolveConfig(ranks=tuple(int(r) for r in z[f"ranks{k}"]), max_sweeps=int(z[f"sweeps{k}"]),
+                             fit_tol=1e-300, pp_enter_tol=0.0)
+        model, trace = tb.tucker_als(t, cfg)
+        fits = np.array([r.fit for r in trace.records])
+        # fit_tol=1e-300 stops only on a bitwise-stationary fit, which rounding decides:
+        # compare the common prefix (both solves are at the fixed point afterwards)
+        m = min(len(fits), len(z[f"fit{k}"]))
+        assert np.abs(fits[:m] - z[f"fit{k}"][:m]).max() < 1e-12
+        for n, f in enumerate(model.factors):
+            assert np.abs(f - z[f"f{k}_{n}"]).max() < 1e-8
+        assert np.abs(model.core.array - z[f"core{k}"]).max() < 1e-8
+
+
+def test_pp_operators_tree():  # tests/test_pp.py:50-83
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((5, 4, 3, 3))
+    anchors = [rand_orth(rng, s, 2) for s in x.shape]
+    st = tb.pp_operators(tb.DenseTensor(x), anchors)
+    assert st.contraction_count == 13
+    ref = oracle.pp_operators(x, anchors)
+    for n in range(4):
+        assert np.abs(st.op_single[n].array - ref.single[n]).max() < 1e-12
+    for key, y in ref.pair.items():
+        assert np.abs(st.op_pair[key].array - y).max() < 1e-12
+
+
+def test_pp_sweep_matches_oracle():  # tests/test_pp.py:93-153
+    rng = np.random.default_rng(12)
+    x = rng.standard_normal((7, 6, 5, 4))
+    ranks = (3, 3, 2, 2)
+    model = tb.t_hosvd(tb.DenseTensor(x), ranks)
+    st = tb.pp_operators(tb.DenseTensor(x), model.factors)
+    moved = tb.hooi_sweep(tb.DenseTensor(x), model)
+    st.set_current(moved.factors)
+    out = tb.pp_sweep(st, moved)
+    ops = oracle.pp_operators(x, model.factors)
+    core_o, fac_o = oracle.pp_sweep(ops, moved.factors)
+    for a, b in zip(out.factors, fac_o):
+        assert np.abs(a - b).max() < 1e-8
+    assert np.abs(out.core.array - core_o).max() < 1e-8
+
+
+# ------------------------------------------------------------------ color.py / codec.py
+def test_colour_f64_matches_reference(golden):
+    z = golden("colour")
+    px = z["fpx"]  # (1, 500, 3); the golden holds pixels[0]
+    assert np.array_equal(tb.rgb_to_ycbcr(tb.ColorImage(px)).pixels[0], z["ycbcr_f"])
+    assert np.abs(tb.rgb_to_ipt(tb.ColorImage(px)).pixels[0] - z["ipt_f"]).max() < 1e-14
+
+
+def test_colour_inverses_roundtrip():  # tests/test_color.py round trips
+    rng = np.random.default_rng(13)
+    px = rng.uniform(0.05, 0.95, size=(8, 9, 3))
+    back = tb.ycbcr_to_rgb(tb.rgb_to_ycbcr(tb.ColorImage(px))).pixels
+    assert np.abs(back - px).max() < 1e-12
+    back2, n = tb.ipt_to_rgb(tb.rgb_to_ipt(tb.ColorImage(px)), count_clamped=True)
+    assert np.abs(back2.pixels - px).max() < 1e-9 and n == 0
+    ref = oracle.ipt_to_rgb(oracle.rgb_to_ipt(px))
+    assert np.abs(back2.pixels - ref).max() < 1e-12
+
+
+def test_colour_u8_kernel_bit_exact(golden):
+    """u8 -> fp32 coding-space tensor equals fp32(reference f64 colour) bit for bit."""
+    z = golden("colour")
+    u8 = z["u8"]
+    for space in ("ycbcr", "ipt"):
+        t = tb.coding_tensor(u8.reshape(1, 1, 1, -1, 3), space).cpu().numpy()
+        got = t.reshape((1, u8.shape[0], 3, 1), order="F")[0, :, :, 0]
+        assert np.array_equal(got, z[f"{space}_u8"].astype(np.float32))
+
+
+def test_quantiser_contracts():  # tests/test_codec.py:57-85
+    rng = np.random.default_rng(14)
+    core = rng.standard_normal((4, 5, 3, 2))
+    fs = [np.eye(s)[:, :r] for s, r in zip((4, 5, 3, 2), (4, 5, 3, 2))]
+    m = tb.TuckerModel(tb.DenseTensor(core), fs, (4, 5, 3, 2))
+    q51 = tb.quantize_core(m, 51)
+    lv, step = oracle.quantize_core(core, 51)
+    assert q51.step == step and np.array_equal(q51.levels, lv) and q51.levels.dtype == np.int64
+    assert tb.quantize_core(m, 45).step == pytest.approx(q51.step / 2, rel=1e-15)
+    deq = tb.dequantize(q51)
+    assert np.abs(deq.core.array - core).max() <= q51.step / 2 + 1e-15
+    assert all(f.dtype == np.float32 for f in q51.factors)
+    z = tb.TuckerModel(tb.DenseTensor(np.zeros((2, 2))), [np.eye(2), np.eye(2)], (2, 2))
+    assert tb.quantize_core(z, 30).step == 1.0
+
+
+def test_launch_counter_advances():
+    n0 = L.launch_count()
+    tb.gram(np.ones((3, 4)))
+    assert L.launch_count() > n0

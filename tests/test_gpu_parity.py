@@ -1,0 +1,80 @@
+"""Hot-path parity: the fused device path (tmb_encode_stack_u8 through the C ABI)
+against the reference goldens (SURVEY.md Appendix B bars) and size-independent
+properties at the full BASELINE config-2 size."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2104_04726_b200 as tb
+from conftest import principal_angle
+from paper_2104_04726_b200.synth import CONFIGS, make_stack
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["c1", "c2q", "c3q"])
+def test_golden_parity(golden, name):
+    z = golden(name)
+    ranks = tuple(int(r) for r in z["ranks"])
+    res = tb.encode_stack(z["images"], str(z["space"]), ranks, int(z["sweeps"]), int(z["qp"]))
+    # factor subspaces: north-star bar 1e-3 rad; we hold 1e-6
+    for n in range(4):
+        assert principal_angle(res.model.factors[n], z[f"factor{n}"]) < 1e-6
+    # relative reconstruction error: bar 1e-4
+    assert abs(res.rel_err - float(z["rel_err"])) < 1e-8
+    # trace: kinds and fits over the common prefix (the reference may stop earlier when its
+    # fit becomes bitwise stationary under fit_tol=1e-300)
+    fits = np.array([r.fit for r in res.trace.records])
+    m = min(len(fits), len(z["trace_fit"]))
+    assert np.abs(fits[:m] - z["trace_fit"][:m]).max() < 1e-9
+    assert [r.kind for r in res.trace.records[:m]] == list(z["trace_kind"][:m])
+    # quantised core: bit-exact except rounding ties (sign-canonicalised columns)
+    signs = [np.sign(np.sum(res.model.factors[n] * z[f"factor{n}"], axis=0)) for n in range(4)]
+    lv = res.levels * np.einsum("i,j,k,l->ijkl", *signs).astype(np.int64)
+    assert float(res.step) == pytest.approx(float(z["step"]), rel=1e-12)
+    diff = lv != z["levels"]
+    if diff.any():
+        q = z["core"] / float(z["step"])
+        tie = np.abs(np.abs(q) - np.floor(np.abs(q)) - 0.5) < 1e-6
+        assert np.all(tie[diff]) and np.abs(lv - z["levels"])[diff].max() <= 1
+    # orthonormal factors (TuckerModel.validate at ORTHO_TOL)
+    res.model.validate()
+
+
+def test_c2_full_size_properties():
+    """BASELINE config 2 at full size: orthonormality, monotone fit, the
+    ||t||^2 - ||core||^2 identity vs the explicit reconstruction, quantiser
+    bounds and bit-reproducibility."""
+    cfg = CONFIGS["c2"]
+    images = make_stack(cfg, seed=0)
+    a = tb.encode_stack(images, cfg.space, cfg.ranks, cfg.sweeps, cfg.qp)
+    b = tb.encode_stack(images, cfg.space, cfg.ranks, cfg.sweeps, cfg.qp)
+    assert np.array_equal(a.levels, b.levels) and a.step == b.step
+    for fa, fb in zip(a.model.factors, b.model.factors):
+        assert np.array_equal(fa, fb)
+    a.model.validate()
+    fits = [r.fit for r in a.trace.records]
+    assert len(fits) == cfg.sweeps + 1
+    assert all(y >= x - 1e-12 for x, y in zip(fits, fits[1:]))
+    # fit via the core identity equals 1 - explicit residual from the reconstruction
+    assert abs((1.0 - a.rel_err) - fits[-1]) < 1e-6
+    core = a.model.core.array
+    assert np.abs(core - a.levels * a.step).max() <= a.step / 2 * (1 + 1e-12)
+    assert np.abs(a.levels).max() == 1024  # 10-bit at qp 39: max|level| = 2^10
+
+
+def test_c1_full_config_exact_k():
+    """BASELINE config 1 (the CPU-runnable case) against its golden, via the
+    f64 drop-in API on the same fp32-rounded tensor the golden used."""
+    import oracle
+
+    z = np.load(__import__("conftest").GOLDEN / "c1.npz")
+    x = oracle.coding_tensor(z["images"], "ycbcr").astype(np.float32).astype(np.float64)
+    cfg = tb.SolveConfig(ranks=(48, 64, 3, 3), max_sweeps=10, fit_tol=1e-300, pp_enter_tol=0.0)
+    model, trace = tb.tucker_als(tb.DenseTensor(x), cfg)
+    for n in range(4):
+        assert principal_angle(model.factors[n], z[f"factor{n}"]) < 1e-6
+    q = tb.quantize_core(model, 51)
+    assert int((q.levels != z["levels"]).sum()) == 0

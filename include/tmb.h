@@ -128,10 +128,11 @@ int tmb_hooi_sweep(tmb_ctx* ctx, const void* x_dev, int dtype, int order, const 
 /* reconstruct (tucker.py:166-171): out F-order dims. */
 int tmb_reconstruct(tmb_ctx* ctx, int order, const int64_t* ranks, const int64_t* dims,
                     const double* core_dev, const double* const* factors_dev, double* out_dev);
-/* tucker_als (tucker.py:331-397): full driver incl. trace, convergence and
- * best-of selection. Pairwise-perturbation sweeps are not implemented yet:
- * if a solve reaches a sweep that would run in the PP phase the call returns
- * TMB_ENOTIMPL (never a silent divergence from the reference trace). */
+/* tucker_als (tucker.py:331-397): full driver incl. trace, convergence,
+ * best-of selection and the pairwise-perturbation phase (PP operators from a
+ * memoised dimension tree, first-order sweeps with the entry deltas, exact
+ * core re-projection, fit-dip rejection and anchor refresh; tucker.py:199-311,
+ * 359-387). */
 int tmb_tucker_als(tmb_ctx* ctx, const void* x_dev, int dtype, int order, const int64_t* dims,
                    const int64_t* ranks, const tmb_solve_cfg* cfg, double* core_dev,
                    double* const* factors_dev, tmb_trace* trace);

@@ -305,6 +305,111 @@ void reconstruct_dev(Ctx& c, const Dims& ranks, const Dims& dims, const double* 
   (void)N;
 }
 
+// ------------------------------------------------------------------ pairwise perturbation
+// tucker.py:199-311. Operators persist across sweeps (own cudaMalloc buffers,
+// outside the per-sweep arena); rebuilt only when the PP phase refreshes.
+struct DevBuf {
+  double* p = nullptr;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) {
+    TMB_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double)));
+  }
+  ~DevBuf() { if (p) cudaFree(p); }
+  DevBuf(DevBuf&& o) noexcept : p(o.p) { o.p = nullptr; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { if (p) cudaFree(p); p = o.p; o.p = nullptr; }
+    return *this;
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+
+struct PPOps {
+  std::vector<DevBuf> anchors;          // device copies of the anchor factors
+  std::vector<std::pair<unsigned, DevBuf>> nodes;  // free-mode bitmask -> operator
+  int count = 0;                        // contractions evaluated (13 for N = 4)
+  const double* find(unsigned m) const {
+    for (const auto& kv : nodes)
+      if (kv.first == m) return kv.second.p;
+    return nullptr;
+  }
+};
+
+static Dims node_dims(const Dims& dims, const Dims& ranks, unsigned free_modes) {
+  Dims d(dims.size());
+  for (size_t n = 0; n < dims.size(); ++n) d[n] = ((free_modes >> n) & 1u) ? dims[n] : ranks[n];
+  return d;
+}
+
+// Memoised dimension tree: the parent of a node re-adds its largest contracted
+// mode, so every node is an ascending contraction (tucker.py:238-252).
+static std::pair<const void*, DType> pp_node(Ctx& c, PPOps& ops, const void* x, DType tx, const Dims& dims,
+                                             const Dims& ranks, unsigned free_modes) {
+  const int N = (int)dims.size();
+  const unsigned all = (1u << N) - 1u;
+  if (free_modes == all) return {x, tx};
+  if (const double* got = ops.find(free_modes)) return {got, F64};
+  int m = N - 1;
+  while ((free_modes >> m) & 1u) --m;
+  const auto parent = pp_node(c, ops, x, tx, dims, ranks, free_modes | (1u << m));
+  DevBuf out((size_t)prod(node_dims(dims, ranks, free_modes), 0, N));
+  ttm_dev(c, parent.first, parent.second, node_dims(dims, ranks, free_modes | (1u << m)), m, ops.anchors[m].p,
+          ranks[m], dims[m], 1, out.p);
+  ops.count++;
+  ops.nodes.emplace_back(free_modes, std::move(out));
+  return {ops.nodes.back().second.p, F64};
+}
+
+static void pp_build(Ctx& c, PPOps& ops, const void* x, DType tx, const Dims& dims, const Dims& ranks,
+                     const std::vector<double*>& anchors) {
+  const int N = (int)dims.size();
+  ops.nodes.clear();
+  ops.anchors.clear();
+  ops.count = 0;
+  for (int n = 0; n < N; ++n) {
+    ops.anchors.emplace_back((size_t)dims[n] * ranks[n]);
+    copy_d(c, ops.anchors.back().p, anchors[n], dims[n] * ranks[n]);
+  }
+  for (int n = 0; n < N; ++n) pp_node(c, ops, x, tx, dims, ranks, 1u << n);                  // op_single
+  for (int i = 0; i < N; ++i)
+    for (int n = i + 1; n < N; ++n) pp_node(c, ops, x, tx, dims, ranks, (1u << i) | (1u << n));  // op_pair
+}
+
+// First-order sweep from the entry deltas (tucker.py:268-311): factors only;
+// the driver re-projects the exact core.
+static void pp_sweep_dev(Ctx& c, PPOps& ops, const void* x, DType tx, const Dims& dims, const Dims& ranks,
+                         const std::vector<double*>& fin, const std::vector<bool>& nonzero,
+                         const std::vector<double*>& fout) {
+  const int N = (int)dims.size();
+  const size_t mk = c.arena.mark();
+  std::vector<double*> delta(N);
+  for (int i = 0; i < N; ++i) {  // d_i = f_i - a_i
+    const int64_t cnt = dims[i] * ranks[i];
+    delta[i] = alloc<double>(c, (size_t)cnt);
+    copy_d(c, delta[i], fin[i], cnt);
+    axpy(c, cnt, -1.0, ops.anchors[i].p, delta[i]);
+  }
+  for (int n = 0; n < N; ++n) {
+    const Dims yd = node_dims(dims, ranks, 1u << n);
+    const int64_t ysz = prod(yd, 0, N);
+    double* y = alloc<double>(c, (size_t)ysz);
+    copy_d(c, y, static_cast<const double*>(pp_node(c, ops, x, tx, dims, ranks, 1u << n).first), ysz);
+    double* tmp = alloc<double>(c, (size_t)ysz);
+    for (int i = 0; i < N; ++i) {
+      if (i == n || !nonzero[i]) continue;
+      const unsigned pm = (1u << i) | (1u << n);
+      const double* pair = static_cast<const double*>(pp_node(c, ops, x, tx, dims, ranks, pm).first);
+      ttm_dev(c, pair, F64, node_dims(dims, ranks, pm), i, delta[i], ranks[i], dims[i], 1, tmp);  // x_i d_i^T
+      axpy(c, ysz, 1.0, tmp, y);
+    }
+    double* G = alloc<double>(c, (size_t)dims[n] * dims[n]);
+    double* vals = alloc<double>(c, (size_t)ranks[n]);
+    mode_gram_dev(c, y, F64, yd, n, G);
+    leading_eigvecs(c, G, dims[n], ranks[n], fout[n], vals);
+  }
+  c.arena.release(mk);
+}
+
 // ------------------------------------------------------------------ driver
 static double fit_from(double tn, double core_sumsq) {
   // tucker.py:181-191 with fro_norm = sqrt(sum of squares)
@@ -360,13 +465,40 @@ void tucker_als_dev(Ctx& c, const void* x, DType tx, const Dims& dims, const Dim
   std::vector<double*>* fc = &fa;
   double* cn = cb;
   std::vector<double*>* fn = &fb;
+  PPOps pp;
+  std::vector<int64_t> frows(dims.begin(), dims.end()), fcols(ranks.begin(), ranks.end());
+  auto read_scalars = [&](int count) {
+    TMB_CUDA(cudaMemcpyAsync(c.host_pinned, scal, sizeof(double) * count, cudaMemcpyDeviceToHost, c.stream));
+    TMB_CUDA(cudaStreamSynchronize(c.stream));
+  };
   for (int sweep = 1; !converged && sweep <= cfg.max_sweeps; ++sweep) {
-    if (phase_pp)
-      throw Error(TMB_ENOTIMPL,
-                  "tucker_als: the solve entered the pairwise-perturbation phase at sweep " + std::to_string(sweep) +
-                      " (max factor change fell below pp_enter_tol); PP sweeps are not implemented on the device "
-                      "path yet -- pass pp_enter_tol=0 to run standard HOOI sweeps");
-    hooi_sweep_dev(c, x, tx, dims, ranks, fc->data(), greedy, cn, fn->data());  // tucker.py:368/373
+    int kind = TMB_KIND_STANDARD;
+    bool have_candidate = false;
+    if (phase_pp) {  // tucker.py:359-371
+      for (int n = 0; n < N; ++n) diff_norms(c, (*fc)[n], pp.anchors[n].p, dims[n] * ranks[n], scal + 2 + 2 * n);
+      read_scalars(2 + 2 * N);
+      double max_rel = 0.0;
+      std::vector<bool> nonzero(N);
+      for (int n = 0; n < N; ++n) {
+        nonzero[n] = c.host_pinned[2 + 2 * n] > 0.0;
+        max_rel = std::max(max_rel, std::sqrt(c.host_pinned[2 + 2 * n]) / std::sqrt(c.host_pinned[3 + 2 * n]));
+      }
+      if (max_rel <= cfg.pp_exit_tol) {
+        pp_sweep_dev(c, pp, x, tx, dims, ranks, *fc, nonzero, *fn);
+        ttmc_dev(c, x, tx, dims, fn->data(), frows.data(), fcols.data(), -1, true, greedy, cn);  // _exact_core
+        sumsq_async(c, cn, F64, Pc, scal);
+        read_scalars(1);
+        have_candidate = !(fit_from(tn, c.host_pinned[0]) < cur_fit - 1e-6);  // PP_DIP_TOL, tucker.py:365-366
+      }
+      if (have_candidate) {
+        kind = TMB_KIND_PP;
+      } else {  // drifted or regressed: refresh with a standard sweep and new anchors
+        hooi_sweep_dev(c, x, tx, dims, ranks, fc->data(), greedy, cn, fn->data());
+        pp_build(c, pp, x, tx, dims, ranks, *fn);
+      }
+    } else {
+      hooi_sweep_dev(c, x, tx, dims, ranks, fc->data(), greedy, cn, fn->data());  // tucker.py:373
+    }
     sumsq_async(c, cn, F64, Pc, scal);
     for (int n = 0; n < N; ++n) diff_norms(c, (*fn)[n], (*fc)[n], dims[n] * ranks[n], scal + 2 + 2 * n);
     TMB_CUDA(cudaMemcpyAsync(c.host_pinned, scal, sizeof(double) * (2 + 2 * N), cudaMemcpyDeviceToHost, c.stream));
@@ -375,14 +507,17 @@ void tucker_als_dev(Ctx& c, const void* x, DType tx, const Dims& dims, const Dim
     for (int n = 0; n < N; ++n)
       change = std::max(change, std::sqrt(c.host_pinned[2 + 2 * n]) / std::sqrt(c.host_pinned[3 + 2 * n]));
     const double new_fit = fit_from(tn, c.host_pinned[0]);
-    rec(TMB_KIND_STANDARD, new_fit, change);
+    rec(kind, new_fit, change);
     if (new_fit > best_fit) {  // tucker.py:382-383 (strict)
       best_fit = new_fit;
       best_idx = sweep;
       copy_d(c, cbest, cn, Pc);
       for (int n = 0; n < N; ++n) copy_d(c, fbest[n], (*fn)[n], dims[n] * ranks[n]);
     }
-    if (cfg.pp_enter_tol > 0 && change < cfg.pp_enter_tol) phase_pp = true;  // tucker.py:385-387
+    if (kind == TMB_KIND_STANDARD && !phase_pp && cfg.pp_enter_tol > 0 && change < cfg.pp_enter_tol) {
+      phase_pp = true;  // tucker.py:385-387
+      pp_build(c, pp, x, tx, dims, ranks, *fn);
+    }
     const bool done = std::fabs(new_fit - cur_fit) < cfg.fit_tol;            // tucker.py:389
     std::swap(cc, cn);
     std::swap(fc, fn);

@@ -1,0 +1,35 @@
+"""C2-shaped TTM / Gram GEMMs through the C ABI (device resident), for A/B timing and ncu captures."""
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+from paper_2104_04726_b200 import _lib as L  # noqa: E402
+
+reps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+which = sys.argv[2] if len(sys.argv) > 2 else "all"
+h = L.ctx()
+dims = (1080, 1920, 3, 10)
+x = torch.rand(int(np.prod(dims)), dtype=torch.float32, device="cuda")
+s1 = torch.rand(1920 * 480, dtype=torch.float64, device="cuda")
+s0 = torch.rand(1080 * 270, dtype=torch.float64, device="cuda")
+y = L.empty_f64(1080 * 1920 * 30)
+cases = {
+    "ttm1": (lambda: L.LIB.tmb_ttm(h, L.ptr(x), L.F32, 4, L.i64s(dims), 1, L.ptr(s1), 480, L.ptr(y)), 2 * 480 * np.prod(dims)),
+    "ttm0": (lambda: L.LIB.tmb_ttm(h, L.ptr(x), L.F32, 4, L.i64s(dims), 0, L.ptr(s0), 270, L.ptr(y)), 2 * 270 * np.prod(dims)),
+    "gram1": (lambda: L.LIB.tmb_mode_gram(h, L.ptr(x), L.F32, 4, L.i64s(dims), 1, L.ptr(y)), 1921 * np.prod(dims)),
+}
+for name, (fn, flops) in cases.items():
+    if which != "all" and which != name:
+        continue
+    ts = []
+    for _ in range(reps):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(); rc = fn(); e.record(); torch.cuda.synchronize()
+        L.check(rc, h)
+        ts.append(s.elapsed_time(e))
+    t = min(ts)
+    print(f"{name}: {t:.3f} ms  {flops / t / 1e9:.1f} TFLOP/s")

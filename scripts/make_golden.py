@@ -134,13 +134,48 @@ def api_cases() -> None:
     print("api cases written")
 
 
+def pp_cases() -> None:
+    """Solves whose traces enter the pairwise-perturbation phase: the reference's
+    DEFAULT SolveConfig on random tensors, and config 1 forced past convergence."""
+    out = {}
+    specs = [(23, (9, 7, 5, 3), (3, 3, 2, 2), {}), (1, (12, 10, 6, 4), (4, 3, 2, 2), {}),
+             (2, (20, 16, 3, 6), (6, 5, 3, 3), {}), (3, (10, 9, 8), (3, 3, 3), {}),
+             (1, (12, 10, 6, 4), (4, 3, 2, 2), {"fit_tol": 1e-9, "max_sweeps": 40})]
+    for k, (seed, dims, ranks, kw) in enumerate(specs):
+        x = np.random.default_rng(seed).standard_normal(dims)
+        model, trace = tucker_als(DenseTensor(x), SolveConfig(ranks=ranks, **kw))
+        out[f"x{k}"] = x
+        out[f"ranks{k}"] = np.array(ranks)
+        out[f"max_sweeps{k}"] = np.array(kw.get("max_sweeps", 50))
+        out[f"fit_tol{k}"] = np.array(kw.get("fit_tol", 1e-5))
+        out[f"kinds{k}"] = np.array("".join(r.kind[0] for r in trace.records))
+        out[f"fit{k}"] = np.array([r.fit for r in trace.records])
+        out[f"converged{k}"] = np.array(trace.converged)
+        out[f"core{k}"] = model.core.array
+        for n, f in enumerate(model.factors):
+            out[f"f{k}_{n}"] = f
+    # config 1, 25 sweeps, fit_tol 1e-12: PP enters around sweep 7
+    z = np.load(OUT / "c1.npz")
+    x = np.asfortranarray(ref_tensor(z["images"], "ycbcr").astype(np.float32).astype(np.float64))
+    model, trace = tucker_als(DenseTensor(x), SolveConfig(ranks=(48, 64, 3, 3), max_sweeps=25, fit_tol=1e-12))
+    out["c1_kinds"] = np.array("".join(r.kind[0] for r in trace.records))
+    out["c1_fit"] = np.array([r.fit for r in trace.records])
+    out["c1_core"] = model.core.array
+    for n, f in enumerate(model.factors):
+        out[f"c1_f{n}"] = f
+    np.savez_compressed(OUT / "pp.npz", **out)
+    print("pp cases written:", [str(out[f"kinds{k}"]) for k in range(len(specs))], str(out["c1_kinds"]))
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
-    names = sys.argv[1:] or (list(CASES) + ["colour", "api"])
+    names = sys.argv[1:] or (list(CASES) + ["colour", "api", "pp"])
     for nm in names:
         if nm == "colour":
             colour_kat()
         elif nm == "api":
             api_cases()
+        elif nm == "pp":
+            pp_cases()
         else:
             run_case(nm)

@@ -20,6 +20,7 @@
 #include <cooperative_groups.h>
 
 #include <cfloat>
+#include <cstdlib>
 
 #include "tmb_internal.cuh"
 
@@ -166,18 +167,23 @@ struct TrdArgs {
   double* d; double* e; double* tau; double* hv;  // hv: n x n, column k = v_k
   double* pbuf;  // 2 x n
   double* part;  // 2 x gridDim
+  int64_t k_end; // stop before step k_end (the cluster kernel continues from there)
 };
 
 __device__ double block_sum_all(double v, double* red) {
-  // result broadcast to all threads; fixed combination order
+  // result broadcast to all threads (red needs 33 slots); fixed combination
+  // order: warp partials -> warp 0 shuffle tree -> red[32]
   v = warp_sum(v);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   __syncthreads();
   if (lane == 0) red[w] = v;
   __syncthreads();
-  double s = 0.0;
-  for (int i = 0; i < nw; ++i) s += red[i];
-  return s;
+  if (w == 0) {
+    const double x = warp_sum(lane < nw ? red[lane] : 0.0);
+    if (lane == 0) red[32] = x;
+  }
+  __syncthreads();
+  return red[32];
 }
 
 // Householder for x[lo..n-1] already in buf: alpha = buf[lo], tail lo+1.. ; writes
@@ -253,14 +259,7 @@ __device__ __forceinline__ double column_pass(double* __restrict__ col, int64_t 
 // Deterministic block sum broadcast to every thread (fixed shuffle tree and
 // fixed warp order), identical in every block for identical inputs.
 __device__ __forceinline__ double block_sum_bcast(double v, double* red) {
-  v = warp_sum(v);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[w] = v;
-  __syncthreads();
-  double s = 0.0;
-  for (int i = 0; i < nw; ++i) s += red[i];
-  return s;
+  return block_sum_all(v, red);
 }
 
 // 256-thread blocks, two per SM (measured faster than one 512-thread block:
@@ -276,7 +275,7 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) k_sytrd(const TrdArgs a) {
   double* wk = sm + n;       // w_k
   double* vn = sm + 2 * n;   // next reflector v_{k+1} (rows >= k+2 valid)
   double* red = sm + 3 * n;  // 32
-  double* sc = red + 32;     // 8
+  double* sc = red + 33;     // 8 (red uses 33 slots)
   const int tid = threadIdx.x, bd = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nw = bd >> 5;
   const int64_t gw = (int64_t)blockIdx.x * nw + warp, GW = (int64_t)gridDim.x * nw;
@@ -306,7 +305,7 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) k_sytrd(const TrdArgs a) {
   }
   grid.sync();
 
-  for (int64_t k = 0; k + 2 < n; ++k) {
+  for (int64_t k = 0; k + 2 < n && k < a.k_end; ++k) {
     const int buf = (int)(k & 1);
     const double* pb = a.pbuf + buf * n;
     const double* pt = a.part + buf * nb;
@@ -728,12 +727,30 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
   const void* kern = (const void*)k_sytrd;
   const int blocks = info.blocks;
   double* part = alloc<double>(c, 2 * (size_t)blocks);
-  TrdArgs ta{A, n, d, e, tau, hv, pbuf, part};
+  // Steps 0..K0-1 grid-wide; the trailing (n-K0-1)-block goes to the cluster
+  // kernel (one cluster barrier per column instead of a grid barrier).
+  static const int64_t tail_env = [] {
+    const char* s = std::getenv("TMB_SYTRD_TAIL");  // A/B switch: max trailing size, 0 = off
+    return s ? std::atoll(s) : (int64_t)-1;
+  }();
+  // Measured (scripts/ab_tail.sh): the cluster kernel wins for whole solves up
+  // to n ~ 400 (n=300: 1.63 vs 1.80 ms) but loses as a tail of larger solves
+  // (n=600: 4.2 vs 3.7 ms), so by default it only takes small matrices whole.
+  const int64_t cap = sytrd_tail_capacity(c);
+  int64_t K0 = (n - 1 <= std::min<int64_t>(cap, 400)) ? 0 : n;
+  if (tail_env >= 0) {
+    const int64_t tail_m = std::min(cap, tail_env);
+    K0 = tail_m >= 2 ? std::max<int64_t>(0, n - 1 - tail_m) : n;
+  }
+  TrdArgs ta{A, n, d, e, tau, hv, pbuf, part, K0};
   void* args[] = {&ta};
   {
     Timed timed(c, TAG_SYTRD, 4.0 / 3.0 * (double)n * n * n);  // dsytrd flop count
-    TMB_CUDA(cudaLaunchCooperativeKernel(kern, blocks, TRD_THREADS, args, smem, c.stream));
-    LAUNCHED("k_sytrd");
+    if (K0 > 0) {
+      TMB_CUDA(cudaLaunchCooperativeKernel(kern, blocks, TRD_THREADS, args, smem, c.stream));
+      LAUNCHED("k_sytrd");
+    }
+    if (K0 < n) sytrd_tail(c, A, n, K0, d, e, tau, hv);
   }
   double* dp = alloc<double>(c, (size_t)n * k);
   double* dm = alloc<double>(c, (size_t)n * k);

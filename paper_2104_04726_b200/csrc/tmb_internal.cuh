@@ -133,6 +133,9 @@ void resid2_async(Ctx& c, const void* t, DType tt, const double* that, int64_t n
 // Dominant-k eigenpairs of a symmetric n x n (column-major) matrix, eigenvalues
 // nonincreasing, columns sign-fixed (tensor.py:183-209). g is not modified.
 void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs, double* vals);
+// Cluster-resident tridiagonalisation of the trailing block from step K0 (k_sytrd_tail.cu).
+int64_t sytrd_tail_capacity(Ctx& c);
+void sytrd_tail(Ctx& c, double* A, int64_t n, int64_t K0, double* d, double* e, double* tau, double* hv);
 
 // ---------------------------------------------------------------- colour (k_color.cu)
 void color_u8(Ctx& c, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, int space, float* out);

@@ -251,7 +251,7 @@ void gemm(Ctx& c, const GemmDesc& d0) {
   // algorithmic flops: 2mnk per product, s(s+1)K for a SYRK
   const double kk = (double)d.K1 * (double)d.K2 * d.batch;
   const double work = d.syrk_upper ? (double)d.M * (d.M + 1) * kk : 2.0 * d.M * d.N * kk;
-  Timed timed(c, TAG_GEMM, work);
+  Timed timed(c, c.gemm_tag, work);
   if (d.ta == F64 && d.tb == F64) launch_t<double, double>(c, a, grid);
   else if (d.ta == F32 && d.tb == F64) launch_t<float, double>(c, a, grid);
   else if (d.ta == F64 && d.tb == F32) launch_t<double, float>(c, a, grid);

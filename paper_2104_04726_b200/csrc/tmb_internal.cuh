@@ -58,7 +58,7 @@ struct KernelTimes {
   struct Rec { int tag; size_t a, b; double work; };
   std::vector<Rec> recs;
 };
-enum TimerTag { TAG_GEMM = 0, TAG_SYTRD, TAG_TRIDIAG, TAG_COLOR, TAG_SMALL, TAG_COUNT };
+enum TimerTag { TAG_GEMM = 0, TAG_SYTRD, TAG_TRIDIAG, TAG_COLOR, TAG_EIG_GEMM, TAG_COUNT };
 
 struct Ctx {
   int device = 0;
@@ -72,6 +72,7 @@ struct Ctx {
   bool timing = false;
   KernelTimes kt;
   double work[TAG_COUNT] = {0};    // algorithmic flops/bytes attributed per tag
+  int gemm_tag = TAG_GEMM;         // TAG_EIG_GEMM while inside the eigen-solver
 };
 
 // RAII: records an event pair around the launches in its scope (if enabled)

@@ -168,22 +168,33 @@ struct TrdArgs {
   double* pbuf;  // 2 x n
   double* part;  // 2 x gridDim
   int64_t k_end; // stop before step k_end (the cluster kernel continues from there)
+  long long* prof;  // optional phase timestamps (TMB_TRD_PROFILE), else nullptr
 };
+
+// Phase timestamps for 3 blocks x 8 sampled steps x 8 phases (diagnostics only).
+#define TRD_PROF(phase)                                                                          \
+  do {                                                                                           \
+    if (a.prof && tid == 0) {                                                                    \
+      const int bs = blockIdx.x == 0 ? 0 : (blockIdx.x == nb / 2 ? 1 : (blockIdx.x == nb - 1 ? 2 : -1)); \
+      const int64_t q4 = (n - 2) / 4;                                                            \
+      const int ss = (k % q4 < 2 && k / q4 < 4) ? (int)(2 * (k / q4) + k % q4) : -1;             \
+      if (bs >= 0 && ss >= 0) a.prof[(bs * 8 + ss) * 8 + (phase)] = clock64();                   \
+    }                                                                                            \
+  } while (0)
 
 __device__ double block_sum_all(double v, double* red) {
   // result broadcast to all threads (red needs 33 slots); fixed combination
   // order: warp partials -> warp 0 shuffle tree -> red[32]
+  // (With 8 warps per block, every thread summing the 8 partials measured
+  // faster than a third barrier for a warp-0 tree.)
   v = warp_sum(v);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   __syncthreads();
   if (lane == 0) red[w] = v;
   __syncthreads();
-  if (w == 0) {
-    const double x = warp_sum(lane < nw ? red[lane] : 0.0);
-    if (lane == 0) red[32] = x;
-  }
-  __syncthreads();
-  return red[32];
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += red[i];
+  return s;
 }
 
 // Householder for x[lo..n-1] already in buf: alpha = buf[lo], tail lo+1.. ; writes
@@ -225,6 +236,10 @@ __device__ __forceinline__ void load_chunk(const double* __restrict__ col, int64
 }
 
 // `cur` holds the first chunk (rows lo+lane+32u), already loaded by the caller.
+// Pipeline depth note (TMB_TRD_PROFILE, ncu): deeper register windows (3-4
+// chunks in flight) spill at the 128-register cap of 2 blocks/SM and measured
+// slower (20.5 vs 17.9 ms at n = 1920); the pass is limited by the three
+// shared-memory vector loads per element and by block-barrier waits.
 __device__ __forceinline__ double column_pass(double* __restrict__ col, int64_t lo, int64_t n, int lane,
                                               const double* __restrict__ vk, const double* __restrict__ wk,
                                               const double* __restrict__ vn, double vjj, double wjj, bool update,
@@ -310,6 +325,7 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) k_sytrd(const TrdArgs a) {
     const double* pb = a.pbuf + buf * n;
     const double* pt = a.part + buf * nb;
     const int64_t c1 = k + 1;
+    TRD_PROF(0);
     // ---- static column ownership (j = gw mod GW): prefetch the first live chunk
     // of this warp's first owned trailing column now, so its L2 latency overlaps
     // the gather / reflector phase instead of starting the fused pass.
@@ -329,6 +345,7 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) k_sytrd(const TrdArgs a) {
     double extra = 0.0;  // large-n tail of the partials
     for (int b = tid + bd; b < nb; b += bd) extra += pt[b];
     const double K = 0.5 * tau_k * block_sum_bcast(pv_part + extra, red);
+    TRD_PROF(1);
     // ---- w_k = p_k - K v_k and the updated column c1 (x) in the same pass
     const double vj = vk[c1], wj = p_c1 - K * vj;
     double s2 = 0.0;
@@ -363,6 +380,7 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) k_sytrd(const TrdArgs a) {
     }
     // ---- next reflector (redundant in every block): dlarfg on x[k+2..]
     const double xn2 = block_sum_bcast(s2, red);
+    TRD_PROF(2);
     if (tid == 0) {
       const double alpha = vn[k + 2];
       double tau = 0.0, beta = alpha, scale = 0.0;
@@ -379,6 +397,7 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) k_sytrd(const TrdArgs a) {
     for (int64_t i = k + 3 + tid; i < n; i += bd) vn[i] *= scale;
     if (tid == 0) vn[k + 2] = 1.0;
     __syncthreads();
+    TRD_PROF(3);
     if (blockIdx.x == 0) {
       if (tid == 0) { a.d[c1] = sc[4]; a.e[c1] = sc[1]; a.tau[c1] = tau_n; }
       double* h = a.hv + n * c1;
@@ -393,12 +412,15 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) k_sytrd(const TrdArgs a) {
       if (lane == 0) pbn[j] = p;
       wpart = fma(p, vn[j], wpart);
     }
+    TRD_PROF(4);
     const double s = block_sum_bcast(lane == 0 ? wpart : 0.0, red);
     if (tid == 0) a.part[(buf ^ 1) * nb + blockIdx.x] = s;
+    TRD_PROF(5);
     // v_k <- v_{k+1}: swap buffers (rows below k+2 are never read again)
     double* t = vk; vk = vn; vn = t;
     tau_k = tau_n;
     grid.sync();
+    TRD_PROF(6);
   }
 }
 
@@ -750,15 +772,37 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
     const int64_t tail_m = std::min(cap, tail_env);
     K0 = tail_m >= 2 ? std::max<int64_t>(0, n - 1 - tail_m) : n;
   }
-  TrdArgs ta{A, n, d, e, tau, hv, pbuf, part, K0};
+  static const bool prof_on = std::getenv("TMB_TRD_PROFILE") != nullptr;
+  long long* prof = nullptr;
+  if (prof_on) {
+    prof = alloc<long long>(c, 3 * 8 * 8);
+    TMB_CUDA(cudaMemsetAsync(prof, 0, sizeof(long long) * 3 * 8 * 8, c.stream));
+  }
+  TrdArgs ta{A, n, d, e, tau, hv, pbuf, part, K0, prof};
   void* args[] = {&ta};
   {
     Timed timed(c, TAG_SYTRD, 4.0 / 3.0 * (double)n * n * n);  // dsytrd flop count
-    if (K0 > 0) {
+    static const bool rows_off = std::getenv("TMB_SYTRD_COLS") != nullptr;  // A/B: force the column kernel
+    if (K0 > 0 && (rows_off || !sytrd_rows(c, A, n, K0, d, e, tau, hv, pbuf))) {
       TMB_CUDA(cudaLaunchCooperativeKernel(kern, blocks, TRD_THREADS, args, smem, c.stream));
       LAUNCHED("k_sytrd");
     }
     if (K0 < n) sytrd_tail(c, A, n, K0, d, e, tau, hv);
+  }
+  if (prof && K0 > 0) {  // diagnostics: mean cycles per phase over the sampled steps/blocks
+    long long h[3 * 8 * 8];
+    TMB_CUDA(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    TMB_CUDA(cudaStreamSynchronize(c.stream));
+    for (int bs = 0; bs < 3; ++bs) {
+      std::fprintf(stderr, "sytrd n=%lld block-slot %d:", (long long)n, bs);
+      for (int ss = 0; ss < 8; ++ss) {
+        const long long* r = h + (bs * 8 + ss) * 8;
+        if (!r[0] || !r[5]) continue;
+        std::fprintf(stderr, " [s%d gather+K %lld wx+s2 %lld house %lld pass %lld red %lld barrier %lld]", ss,
+                     r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], r[5] - r[4], r[6] ? r[6] - r[5] : -1);
+      }
+      std::fprintf(stderr, "\n");
+    }
   }
   double* dp = alloc<double>(c, (size_t)n * k);
   double* dm = alloc<double>(c, (size_t)n * k);

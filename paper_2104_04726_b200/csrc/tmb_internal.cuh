@@ -134,6 +134,10 @@ void resid2_async(Ctx& c, const void* t, DType tt, const double* that, int64_t n
 // Dominant-k eigenpairs of a symmetric n x n (column-major) matrix, eigenvalues
 // nonincreasing, columns sign-fixed (tensor.py:183-209). g is not modified.
 void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs, double* vals);
+// Row-partitioned cooperative tridiagonalisation for n <= 2048 (k_sytrd_rows.cu);
+// false if n is out of its range.
+bool sytrd_rows(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* e, double* tau, double* hv,
+                double* pbuf);
 // Cluster-resident tridiagonalisation of the trailing block from step K0 (k_sytrd_tail.cu).
 int64_t sytrd_tail_capacity(Ctx& c);
 void sytrd_tail(Ctx& c, double* A, int64_t n, int64_t K0, double* d, double* e, double* tau, double* hv);

@@ -26,7 +26,6 @@ namespace cg = cooperative_groups;
 namespace tmb {
 namespace {
 
-constexpr int RW_THREADS = 256;
 
 struct RowArgs {
   double* A;
@@ -43,23 +42,25 @@ __device__ __forceinline__ double wsum(double v) {
 // Block sum, broadcast; fixed order (8 warps). One barrier per call: the warp
 // partials alternate between two 8-slot buffers, so a buffer is only rewritten
 // after another call's barrier has passed every reader.
+template <int NW>
 __device__ __forceinline__ double bsum(double v, double* red, int& phase) {
   v = wsum(v);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double* r = red + 8 * phase;
+  double* r = red + NW * phase;
   phase ^= 1;
   if (lane == 0) r[w] = v;
   __syncthreads();
   double s = 0.0;
 #pragma unroll
-  for (int i = 0; i < RW_THREADS / 32; ++i) s += r[i];
+  for (int i = 0; i < NW; ++i) s += r[i];
   return s;
 }
 
 // RPT: rows per thread (n <= 256 RPT); RW_CB: owned columns whose loads are
 // issued together (memory-level parallelism vs registers).
-template <int RPT, int RW_CB>
-__global__ void __launch_bounds__(RW_THREADS, 2) k_sytrd_rows(const RowArgs a) {
+template <int RPT, int RW_CB, int RW_THREADS>
+__global__ void __launch_bounds__(RW_THREADS, 512 / RW_THREADS) k_sytrd_rows(const RowArgs a) {
+  constexpr int NW = RW_THREADS / 32;
   cg::grid_group grid = cg::this_grid();
   const int64_t n = a.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -68,8 +69,8 @@ __global__ void __launch_bounds__(RW_THREADS, 2) k_sytrd_rows(const RowArgs a) {
   extern __shared__ double sm[];
   double* vks = sm;            // n: v_k (full, for per-column scalars)
   double* wks = sm + n;        // n: w_k
-  double* part = sm + 2 * n;   // 8 warps x 64 columns: per-warp partial dots
-  double* red = part + 8 * 64; // 2 x 8
+  double* part = sm + 2 * n;   // NW warps x 64 columns: per-warp partial dots
+  double* red = part + NW * 64; // 2 x NW
   int rph = 0;
 
   double vr[RPT], wr[RPT], nr[RPT];  // v_k, w_k, v_{k+1} on own rows
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(RW_THREADS, 2) k_sytrd_rows(const RowArgs a) {
     if (i >= 2 && i < n) s2 = fma(x0[u], x0[u], s2);
   }
   alpha = A[1];
-  double xn2 = bsum(s2, red, rph);
+  double xn2 = bsum<NW>(s2, red, rph);
   double tau_k = 0.0, beta = alpha, scale = 0.0;
   if (xn2 > 0.0) {
     const double nrm = sqrt(alpha * alpha + xn2);
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(RW_THREADS, 2) k_sytrd_rows(const RowArgs a) {
       if (j < n) {
         double s = 0.0;
 #pragma unroll
-        for (int w = 0; w < RW_THREADS / 32; ++w) s += part[w * 64 + tid];
+        for (int w = 0; w < NW; ++w) s += part[w * 64 + tid];
         a.pbuf[j] = tau_k * s;
       }
     }
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(RW_THREADS, 2) k_sytrd_rows(const RowArgs a) {
     double pv = 0.0;
 #pragma unroll
     for (int u = 0; u < RPT; ++u) pv = fma(pp[u], vr[u], pv);  // rows < c1 contribute 0
-    const double K = 0.5 * tau_k * bsum(pv, red, rph);
+    const double K = 0.5 * tau_k * bsum<NW>(pv, red, rph);
     // ---- w_k and the updated column c1 on own rows
     const double v_c1 = vks[c1], v_k2 = vks[k + 2];
     const double w_c1 = p_c1 - K * v_c1, w_k2 = p_k2 - K * v_k2;
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(RW_THREADS, 2) k_sytrd_rows(const RowArgs a) {
       }
       break;
     }
-    xn2 = bsum(s2, red, rph);
+    xn2 = bsum<NW>(s2, red, rph);
     // ---- next reflector, every thread redundantly (alpha = x[k+2])
     alpha = a_k2 - v_k2 * w_c1 - w_k2 * v_c1;
     double tau_n = 0.0;
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(RW_THREADS, 2) k_sytrd_rows(const RowArgs a) {
       if (j < n) {
         double s = 0.0;
 #pragma unroll
-        for (int w = 0; w < RW_THREADS / 32; ++w) s += part[w * 64 + tid];
+        for (int w = 0; w < NW; ++w) s += part[w * 64 + tid];
         pbn[j] = tau_n * s;
       }
     }
@@ -275,27 +276,42 @@ struct RowsInfo { int blocks = 0; int64_t n = -1; };
 // caller then uses the column-per-warp kernel).
 bool sytrd_rows(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* e, double* tau, double* hv,
                 double* pbuf) {
-  if (n > 2048 || n < 3) return false;  // RPT <= 8 keeps the row registers under the 2-block cap
-  const int rpt = (int)ceil_div(n, RW_THREADS);
+  if (n > 2048 || n < 3) return false;  // rows per thread <= 8 (256 threads) / 4 (512 threads)
   static const int cb_env = [] {
     const char* s = std::getenv("TMB_ROWS_CB");  // A/B: columns per load batch
     return s ? std::atoi(s) : 0;
   }();
+  static const int nt_env = [] {
+    const char* s = std::getenv("TMB_ROWS_NT");  // A/B: 256 or 512 threads per block
+    return s ? std::atoi(s) : 0;
+  }();
   using KFn = void (*)(RowArgs);
   KFn kern;
-  int slot;
-  // defaults from scripts/ab_rows.sh: CB 2 / 2 / 1 / 2 for RPT 2 / 4 / 6 / 8
-  if (rpt <= 2) { kern = cb_env == 1 ? k_sytrd_rows<2, 1> : (cb_env == 4 ? k_sytrd_rows<2, 4> : k_sytrd_rows<2, 2>); slot = 0; }
-  else if (rpt <= 4) { kern = cb_env == 1 ? k_sytrd_rows<4, 1> : (cb_env == 4 ? k_sytrd_rows<4, 4> : k_sytrd_rows<4, 2>); slot = 1; }
-  else if (rpt <= 6) { kern = cb_env == 2 ? k_sytrd_rows<6, 2> : (cb_env == 4 ? k_sytrd_rows<6, 4> : k_sytrd_rows<6, 1>); slot = 2; }
-  else { kern = cb_env == 1 ? k_sytrd_rows<8, 1> : k_sytrd_rows<8, 2>; slot = 3; }
-  const size_t smem = sizeof(double) * (2 * n + 8 * 64 + 16);
-  static RowsInfo info[4];
+  int slot, nt;
+  // measured (scripts/ab_rows.sh): 512 threads win only for large n (n=1920:
+  // 15.2 vs 16.2 ms; n=1080: 7.3 vs 6.9 ms)
+  const bool big_blocks = nt_env == 512 || (nt_env == 0 && n > 1536);
+  if (big_blocks) {
+    nt = 512;
+    const int rpt = (int)ceil_div(n, 512);
+    if (rpt <= 2) { kern = cb_env == 1 ? k_sytrd_rows<2, 1, 512> : k_sytrd_rows<2, 2, 512>; slot = 4; }
+    else { kern = cb_env == 1 ? k_sytrd_rows<4, 1, 512> : k_sytrd_rows<4, 2, 512>; slot = 5; }
+  } else {
+    nt = 256;
+    const int rpt = (int)ceil_div(n, 256);
+    // defaults from scripts/ab_rows.sh: CB 2 / 2 / 1 / 2 for RPT 2 / 4 / 6 / 8
+    if (rpt <= 2) { kern = cb_env == 1 ? k_sytrd_rows<2, 1, 256> : k_sytrd_rows<2, 2, 256>; slot = 0; }
+    else if (rpt <= 4) { kern = cb_env == 1 ? k_sytrd_rows<4, 1, 256> : k_sytrd_rows<4, 2, 256>; slot = 1; }
+    else if (rpt <= 6) { kern = cb_env == 2 ? k_sytrd_rows<6, 2, 256> : k_sytrd_rows<6, 1, 256>; slot = 2; }
+    else { kern = cb_env == 1 ? k_sytrd_rows<8, 1, 256> : k_sytrd_rows<8, 2, 256>; slot = 3; }
+  }
+  const size_t smem = sizeof(double) * (2 * n + (nt / 32) * 64 + 2 * (nt / 32));
+  static RowsInfo info[6];
   if (info[slot].n != n) {
     TMB_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)std::max<size_t>(smem, 48 * 1024)));
     int per_sm = 0;
-    TMB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kern, RW_THREADS, smem));
+    TMB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kern, nt, smem));
     if (per_sm < 1) return false;
     // at most 64 owned columns per block (the partial array), ~n/NB per block
     const int64_t need = ceil_div(n, 64);
@@ -306,7 +322,7 @@ bool sytrd_rows(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
   }
   RowArgs ra{A, n, k_end, d, e, tau, hv, pbuf};
   void* args[] = {&ra};
-  TMB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, info[slot].blocks, RW_THREADS, args, smem, c.stream));
+  TMB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, info[slot].blocks, nt, args, smem, c.stream));
   c.launches++;
   check_launch("k_sytrd_rows");
   return true;

@@ -18,12 +18,15 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 INCLUDE = PKG.parent / "include"
-BUILD = PKG / "build"
-LIB = PKG / "libtmb.so"
+# TMB_NVCC_FLAGS / TMB_BUILD_DIR / TMB_LIB_OUT: extra flags and output paths for
+# A/B variant builds (scripts/ab_*.sh); defaults build the in-tree library.
+BUILD = Path(os.environ.get("TMB_BUILD_DIR", PKG / "build"))
+LIB = Path(os.environ.get("TMB_LIB_OUT", PKG / "libtmb.so"))
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
-                     "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills", f"-I{INCLUDE}"]
+                     "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills", f"-I{INCLUDE}",
+                     *os.environ.get("TMB_NVCC_FLAGS", "").split()]
 
 
 def nvcc() -> str:
@@ -48,7 +51,7 @@ def _compile(src: Path, verbose: bool) -> Path:
 
 
 def build(verbose: bool = False) -> Path:
-    BUILD.mkdir(exist_ok=True)
+    BUILD.mkdir(parents=True, exist_ok=True)
     sources = sorted(CSRC.glob("*.cu"))
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), sources))

@@ -9,12 +9,13 @@ present every compute call raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 import numpy as np
 
-_PATH = Path(__file__).resolve().parent / "libtmb.so"
+_PATH = Path(os.environ.get("TMB_LIB", Path(__file__).resolve().parent / "libtmb.so"))
 if not _PATH.exists():
     raise ImportError(
         f"{_PATH} is not built; run `python paper_2104_04726_b200/_build.py` "

@@ -655,14 +655,23 @@ static void orthonormalize(Ctx& c, double* x, int64_t n, int64_t k) {
   c.arena.release(mk);
 }
 
-constexpr int WY_NB = 64;
+// Reflectors per compact-WY panel. 64 and 128 measured within 1% of each other
+// (scripts/ab_wy.sh); TMB_WY_NB selects 32/64/128 for A/B runs.
+static int wy_nb() {
+  static const int v = [] {
+    const char* s = std::getenv("TMB_WY_NB");
+    const int x = s ? std::atoi(s) : 64;
+    return (x == 32 || x == 64 || x == 128) ? x : 64;
+  }();
+  return v;
+}
 
 // x <- H_0 H_1 ... H_{n-3} x by compact-WY panels of WY_NB reflectors, last
 // panel first: x <- x - (V_p T_p) (V_p^T x). hv is n x hv_cols with zero
 // columns past the last reflector; tau is zero-padded likewise.
 static void backtransform(Ctx& c, const double* hv, const double* tau, int64_t n, int64_t hv_cols, int64_t k,
                           double* x) {
-  const int nb = WY_NB;
+  const int nb = wy_nb();
   const int np = (int)(hv_cols / nb);
   const size_t mk = c.arena.mark();
   double* S = alloc<double>(c, (size_t)np * nb * nb);
@@ -676,6 +685,11 @@ static void backtransform(Ctx& c, const double* hv, const double* tau, int64_t n
     g.B = hv; g.sBn = n; g.sBk1 = 1; g.sBb = n * nb;
     g.C = S; g.sCm = 1; g.sCn = nb; g.sCb = nb * nb;
     gemm(c, g);
+  }
+  static bool larft_attr = false;
+  if (!larft_attr) {
+    TMB_CUDA(cudaFuncSetAttribute(k_larft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * 128 * 128)));
+    larft_attr = true;
   }
   k_larft<<<np, nb, sizeof(double) * nb * nb, c.stream>>>(S, tau, nb, T);
   LAUNCHED("k_larft");
@@ -731,7 +745,7 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
   double* A = alloc<double>(c, (size_t)n * n);
   // Householder vectors: columns 0..n-3 written by k_sytrd, the rest (up to a
   // whole number of WY panels) stay zero, as do their tau entries.
-  const int64_t hv_cols = ceil_div(n, WY_NB) * WY_NB;
+  const int64_t hv_cols = ceil_div(n, wy_nb()) * wy_nb();
   double* hv = alloc<double>(c, (size_t)n * hv_cols);
   double* d = alloc<double>(c, n);
   double* e = alloc<double>(c, n);

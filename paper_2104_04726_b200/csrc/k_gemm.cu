@@ -20,18 +20,33 @@
 namespace tmb {
 namespace {
 
-constexpr int BM = 128, BN = 64, BK = 16, ST = 3, NT = 256;
+#ifndef TMB_GEMM_ST
+#define TMB_GEMM_ST 3
+#endif
+constexpr int BM = 128, BN = 64, BK = 16, ST = TMB_GEMM_ST, NT = 256;
 
 template <typename T> struct Pad;
 template <> struct Pad<double> { static constexpr int v = 4; };  // 132 = 4 mod 16 (8B banks)
 template <> struct Pad<float> { static constexpr int v = 8; };   // 136 = 8 mod 32 (4B banks)
 
+// Shared-memory image of one ROWS x BK operand tile. MF ("rows fast": the
+// operand's row index has unit global stride) stores [k][row]; otherwise the
+// k index is the contiguous one and the tile is stored [row][k]. Both pads keep
+// the DMMA fragment reads (lanes g = row, tig = k) conflict-free and the
+// 16-byte cp.async destinations aligned.
+template <typename T, bool MF, int ROWS>
+struct Tile {
+  static constexpr int LD = MF ? ROWS + Pad<T>::v : BK + 4;
+  static constexpr int SIZE = MF ? BK * LD : ROWS * LD;
+  __device__ static constexpr int at(int row, int k) { return MF ? k * LD + row : row * LD + k; }
+};
+
 struct KArgs {
   int64_t M, N, K1, K2;
   int batch, splits;
   int64_t kt_total, kt1;
-  const void* A; int64_t sAm, sAk1, sAk2, sAb; int a_mfast;
-  const void* B; int64_t sBn, sBk1, sBk2, sBb; int b_nfast;
+  const void* A; int64_t sAm, sAk1, sAk2, sAb; int a_vec;
+  const void* B; int64_t sBn, sBk1, sBk2, sBb; int b_vec;
   double* C; int64_t sCm, sCn, sCb;
   double alpha, beta;
   double* part;
@@ -42,10 +57,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// cp.async with zero fill: `bytes` (<= BYTES) are read, the rest of the
+// destination is zeroed; bytes == 0 reads nothing (ragged tile edges).
 template <int BYTES>
-__device__ __forceinline__ void cp_async_z(uint32_t s, const void* g, bool valid) {
-  int sz = valid ? BYTES : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(g), "n"(BYTES), "r"(sz));
+__device__ __forceinline__ void cp_async_z(uint32_t s, const void* g, int bytes) {
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(g), "r"(bytes));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(g), "n"(BYTES), "r"(bytes));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -59,12 +78,51 @@ __device__ __forceinline__ void dmma(double (&c)[4], const double (&a)[4], const
       : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
 }
 
-template <typename TA, typename TB>
+// Per-thread copy plan of one operand: V-element chunks (V = 16 B / element
+// when the contiguous index is 16-byte aligned, else 1), each thread owning
+// NIT chunks at a fixed fast coordinate and a slow coordinate stepping by
+// SSTEP -- so a k-tile costs one pointer add per chunk, no index division.
+template <typename T, bool MF, int ROWS, int V>
+struct Plan {
+  static constexpr int FAST = MF ? ROWS : BK;     // extent of the contiguous index
+  static constexpr int CPR = FAST / V;             // chunks per slow line
+  static constexpr int SSTEP = NT / CPR;           // slow-coordinate step per chunk
+  static constexpr int NIT = ROWS * BK / V / NT;
+  static_assert(NIT >= 1 && NT % CPR == 0, "tile/thread mismatch");
+  int64_t off;    // element offset of chunk 0 relative to the k-tile origin
+  int64_t step;   // element offset between consecutive chunks
+  int fast, slow0;
+  __device__ Plan(int tid, int64_t s_row, int64_t s_k1) {
+    fast = (tid % CPR) * V;
+    slow0 = tid / CPR;
+    const int64_t s_fast = MF ? s_row : s_k1, s_slow = MF ? s_k1 : s_row;
+    off = fast * s_fast + slow0 * s_slow;
+    step = SSTEP * s_slow;
+  }
+  // rrem / krem: rows and k left inside the tile (clamped to the tile extents).
+  __device__ __forceinline__ void issue(T* dst, const T* src, int rrem, int krem) const {
+    const int frem = (MF ? rrem : krem) - fast, srem = MF ? krem : rrem;
+    const int nb = (frem >= V ? V : (frem > 0 ? frem : 0)) * (int)sizeof(T);
+    const T* g = src + off;
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int slow = slow0 + it * SSTEP;
+      const bool ok = nb > 0 && slow < srem;
+      const int row = MF ? fast : slow, k = MF ? slow : fast;
+      cp_async_z<V * sizeof(T)>(smem_u32(dst + Tile<T, MF, ROWS>::at(row, k)), ok ? g + it * step : src,
+                                ok ? nb : 0);
+    }
+  }
+};
+
+template <typename TA, typename TB, bool AMF, bool BNF>
 __global__ void __launch_bounds__(NT, 2) k_gemm_dmma(const KArgs p) {
-  constexpr int LDA = BM + Pad<TA>::v, LDB = BN + Pad<TB>::v;
+  using TlA = Tile<TA, AMF, BM>;
+  using TlB = Tile<TB, BNF, BN>;
+  constexpr int VA = 16 / sizeof(TA), VB = 16 / sizeof(TB);
   extern __shared__ __align__(16) unsigned char smem[];
   TA* sA = reinterpret_cast<TA*>(smem);
-  TB* sB = reinterpret_cast<TB*>(smem + sizeof(TA) * ST * BK * LDA);
+  TB* sB = reinterpret_cast<TB*>(smem + sizeof(TA) * ST * TlA::SIZE);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tig = lane & 3;
@@ -75,33 +133,28 @@ __global__ void __launch_bounds__(NT, 2) k_gemm_dmma(const KArgs p) {
   const int64_t per = (p.kt_total + p.splits - 1) / p.splits;
   const int64_t kb = split * per;
   const int64_t ke = kb + per < p.kt_total ? kb + per : p.kt_total;
-  const TA* A = static_cast<const TA*>(p.A) + b * p.sAb;
-  const TB* B = static_cast<const TB*>(p.B) + b * p.sBb;
+  const TA* A = static_cast<const TA*>(p.A) + b * p.sAb + m0 * p.sAm;
+  const TB* B = static_cast<const TB*>(p.B) + b * p.sBb + n0 * p.sBn;
+  const int arem = (int)(p.M - m0 < BM ? p.M - m0 : BM);
+  const int brem = (int)(p.N - n0 < BN ? p.N - n0 : BN);
 
-  auto load = [&](int stage, int64_t kt) {
-    const int64_t k2 = kt / p.kt1, k1b = (kt % p.kt1) * BK;
-    TA* dA = sA + stage * BK * LDA;
-    TB* dB = sB + stage * BK * LDB;
-#pragma unroll
-    for (int it = 0; it < BM * BK / NT; ++it) {
-      const int e = tid + it * NT;
-      int m, k;
-      if (p.a_mfast) { m = e % BM; k = e / BM; } else { k = e % BK; m = e / BK; }
-      const int64_t gm = m0 + m, gk = k1b + k;
-      const bool v = gm < p.M && gk < p.K1;
-      const TA* src = v ? A + gm * p.sAm + gk * p.sAk1 + k2 * p.sAk2 : A;
-      cp_async_z<sizeof(TA)>(smem_u32(dA + k * LDA + m), src, v);
-    }
-#pragma unroll
-    for (int it = 0; it < BN * BK / NT; ++it) {
-      const int e = tid + it * NT;
-      int n, k;
-      if (p.b_nfast) { n = e % BN; k = e / BN; } else { k = e % BK; n = e / BK; }
-      const int64_t gn = n0 + n, gk = k1b + k;
-      const bool v = gn < p.N && gk < p.K1;
-      const TB* src = v ? B + gn * p.sBn + gk * p.sBk1 + k2 * p.sBk2 : B;
-      cp_async_z<sizeof(TB)>(smem_u32(dB + k * LDB + n), src, v);
-    }
+  const Plan<TA, AMF, BM, VA> pav(tid, p.sAm, p.sAk1);
+  const Plan<TA, AMF, BM, 1> pas(tid, p.sAm, p.sAk1);
+  const Plan<TB, BNF, BN, VB> pbv(tid, p.sBn, p.sBk1);
+  const Plan<TB, BNF, BN, 1> pbs(tid, p.sBn, p.sBk1);
+
+  // k-tile cursor of the next load: (k1 offset, slab index), advanced without division
+  int64_t lk1 = (kb % p.kt1) * BK, lk2 = kb / p.kt1;
+  auto load = [&](int stage) {
+    const int krem = (int)(p.K1 - lk1 < BK ? p.K1 - lk1 : BK);
+    const TA* ga = A + lk1 * p.sAk1 + lk2 * p.sAk2;
+    const TB* gb = B + lk1 * p.sBk1 + lk2 * p.sBk2;
+    if (p.a_vec) pav.issue(sA + stage * TlA::SIZE, ga, arem, krem);
+    else pas.issue(sA + stage * TlA::SIZE, ga, arem, krem);
+    if (p.b_vec) pbv.issue(sB + stage * TlB::SIZE, gb, brem, krem);
+    else pbs.issue(sB + stage * TlB::SIZE, gb, brem, krem);
+    lk1 += BK;
+    if (lk1 >= p.K1) { lk1 = 0; ++lk2; }
   };
 
   double acc[2][4][4];
@@ -114,33 +167,34 @@ __global__ void __launch_bounds__(NT, 2) k_gemm_dmma(const KArgs p) {
 
 #pragma unroll
   for (int s = 0; s < ST - 1; ++s) {
-    if (kb + s < ke) load(s, kb + s);
+    if (kb + s < ke) load(s);
     cp_commit();
   }
+  int stage = 0;
   for (int64_t kt = kb; kt < ke; ++kt) {
-    const int i = (int)(kt - kb);
     cp_wait<ST - 2>();
     __syncthreads();
-    if (kt + ST - 1 < ke) load((i + ST - 1) % ST, kt + ST - 1);
+    if (kt + ST - 1 < ke) load(stage == 0 ? ST - 1 : stage - 1);
     cp_commit();
-    const TA* cA = sA + (i % ST) * BK * LDA;
-    const TB* cB = sB + (i % ST) * BK * LDB;
+    const TA* cA = sA + stage * TlA::SIZE;
+    const TB* cB = sB + stage * TlB::SIZE;
+    stage = stage + 1 == ST ? 0 : stage + 1;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 8) {
       double af[2][4], bf[4][2];
 #pragma unroll
       for (int ii = 0; ii < 2; ++ii) {
         const int mb = wm * 32 + ii * 16 + g;
-        af[ii][0] = (double)cA[(kk + tig) * LDA + mb];
-        af[ii][1] = (double)cA[(kk + tig) * LDA + mb + 8];
-        af[ii][2] = (double)cA[(kk + tig + 4) * LDA + mb];
-        af[ii][3] = (double)cA[(kk + tig + 4) * LDA + mb + 8];
+        af[ii][0] = (double)cA[TlA::at(mb, kk + tig)];
+        af[ii][1] = (double)cA[TlA::at(mb + 8, kk + tig)];
+        af[ii][2] = (double)cA[TlA::at(mb, kk + tig + 4)];
+        af[ii][3] = (double)cA[TlA::at(mb + 8, kk + tig + 4)];
       }
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
         const int nb = wn * 32 + jj * 8 + g;
-        bf[jj][0] = (double)cB[(kk + tig) * LDB + nb];
-        bf[jj][1] = (double)cB[(kk + tig + 4) * LDB + nb];
+        bf[jj][0] = (double)cB[TlB::at(nb, kk + tig)];
+        bf[jj][1] = (double)cB[TlB::at(nb, kk + tig + 4)];
       }
 #pragma unroll
       for (int ii = 0; ii < 2; ++ii)
@@ -191,18 +245,34 @@ __global__ void k_mirror(double* g, int64_t n, int batch, int64_t sb) {
   }
 }
 
-template <typename TA, typename TB>
+template <typename TA, typename TB, bool AMF, bool BNF>
 void launch_t(Ctx& c, const KArgs& a, dim3 grid) {
-  constexpr int LDA = BM + Pad<TA>::v, LDB = BN + Pad<TB>::v;
-  const size_t smem = (size_t)ST * BK * (LDA * sizeof(TA) + LDB * sizeof(TB));
+  const size_t smem = (size_t)ST * (Tile<TA, AMF, BM>::SIZE * sizeof(TA) + Tile<TB, BNF, BN>::SIZE * sizeof(TB));
   static bool attr = false;
   if (!attr) {
-    TMB_CUDA(cudaFuncSetAttribute(k_gemm_dmma<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TMB_CUDA(cudaFuncSetAttribute(k_gemm_dmma<TA, TB, AMF, BNF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
     attr = true;
   }
-  k_gemm_dmma<TA, TB><<<grid, NT, smem, c.stream>>>(a);
+  k_gemm_dmma<TA, TB, AMF, BNF><<<grid, NT, smem, c.stream>>>(a);
   c.launches++;
   check_launch("k_gemm_dmma");
+}
+
+template <typename TA, typename TB>
+void launch_l(Ctx& c, const KArgs& a, dim3 grid, bool amf, bool bnf) {
+  if (amf && bnf) launch_t<TA, TB, true, true>(c, a, grid);
+  else if (amf) launch_t<TA, TB, true, false>(c, a, grid);
+  else if (bnf) launch_t<TA, TB, false, true>(c, a, grid);
+  else launch_t<TA, TB, false, false>(c, a, grid);
+}
+
+// 16-byte chunks along the contiguous index need the base and every other
+// stride to be multiples of the chunk (in elements).
+bool vec_ok(const void* base, int elem, int64_t s_other1, int64_t s_other2, int64_t s_batch) {
+  const int64_t v = 16 / elem;
+  return reinterpret_cast<uintptr_t>(base) % 16 == 0 && s_other1 % v == 0 && s_other2 % v == 0 &&
+         s_batch % v == 0;
 }
 
 }  // namespace
@@ -227,8 +297,13 @@ void gemm(Ctx& c, const GemmDesc& d0) {
   a.kt_total = a.kt1 * a.K2;
   a.A = d.A; a.sAm = d.sAm; a.sAk1 = d.sAk1; a.sAk2 = d.sAk2; a.sAb = d.sAb;
   a.B = d.B; a.sBn = d.sBn; a.sBk1 = d.sBk1; a.sBk2 = d.sBk2; a.sBb = d.sBb;
-  a.a_mfast = (d.sAm == 1) ? 1 : (d.sAk1 == 1 ? 0 : 1);
-  a.b_nfast = (d.sBn == 1) ? 1 : (d.sBk1 == 1 ? 0 : 1);
+  const bool amf = (d.sAm == 1) ? true : (d.sAk1 != 1);
+  const bool bnf = (d.sBn == 1) ? true : (d.sBk1 != 1);
+  const int ea = d.ta == F64 ? 8 : 4, eb = d.tb == F64 ? 8 : 4;
+  a.a_vec = (amf ? d.sAm == 1 : d.sAk1 == 1) &&
+            vec_ok(d.A, ea, amf ? d.sAk1 : d.sAm, d.K2 > 1 ? d.sAk2 : 0, d.batch > 1 ? d.sAb : 0);
+  a.b_vec = (bnf ? d.sBn == 1 : d.sBk1 == 1) &&
+            vec_ok(d.B, eb, bnf ? d.sBk1 : d.sBn, d.K2 > 1 ? d.sBk2 : 0, d.batch > 1 ? d.sBb : 0);
   a.C = d.C; a.sCm = d.sCm; a.sCn = d.sCn; a.sCb = d.sCb;
   a.alpha = d.alpha; a.beta = d.beta; a.syrk = d.syrk_upper ? 1 : 0;
   const int64_t tn = ceil_div(d.N, BN), tm = ceil_div(d.M, BM);
@@ -252,10 +327,10 @@ void gemm(Ctx& c, const GemmDesc& d0) {
   const double kk = (double)d.K1 * (double)d.K2 * d.batch;
   const double work = d.syrk_upper ? (double)d.M * (d.M + 1) * kk : 2.0 * d.M * d.N * kk;
   Timed timed(c, c.gemm_tag, work);
-  if (d.ta == F64 && d.tb == F64) launch_t<double, double>(c, a, grid);
-  else if (d.ta == F32 && d.tb == F64) launch_t<float, double>(c, a, grid);
-  else if (d.ta == F64 && d.tb == F32) launch_t<double, float>(c, a, grid);
-  else launch_t<float, float>(c, a, grid);
+  if (d.ta == F64 && d.tb == F64) launch_l<double, double>(c, a, grid, amf, bnf);
+  else if (d.ta == F32 && d.tb == F64) launch_l<float, double>(c, a, grid, amf, bnf);
+  else if (d.ta == F64 && d.tb == F32) launch_l<double, float>(c, a, grid, amf, bnf);
+  else launch_l<float, float>(c, a, grid, amf, bnf);
   if (splits > 1) {
     const int64_t total = (int64_t)d.batch * d.M * d.N;
     const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 8LL * c.num_sms);

@@ -50,10 +50,14 @@ __device__ __forceinline__ double bsum(double v, double* red, int& phase) {
   phase ^= 1;
   if (lane == 0) r[w] = v;
   __syncthreads();
-  double s = 0.0;
+  double t[NW];
 #pragma unroll
-  for (int i = 0; i < NW; ++i) s += r[i];
-  return s;
+  for (int i = 0; i < NW; ++i) t[i] = r[i];
+#pragma unroll
+  for (int h = NW / 2; h > 0; h >>= 1)
+#pragma unroll
+    for (int i = 0; i < h; ++i) t[i] += t[i + h];  // pairwise tree: depth log2(NW)
+  return t[0];
 }
 
 // RPT: rows per thread (n <= 256 RPT); RW_CB: owned columns whose loads are
@@ -268,15 +272,341 @@ __global__ void __launch_bounds__(RW_THREADS, 512 / RW_THREADS) k_sytrd_rows(con
   }
 }
 
+
+// Shared-memory-resident variant (n <= ~1990 on 148 SMs): block b keeps its
+// owned columns j = jb + NB q in SHARED memory for the whole reduction, so the
+// fused update+symv pass streams shared memory instead of L2 (the L2 variant
+// above spends most of a step in dependent L2 round trips). Only what other
+// blocks read goes to global: p_{k+1} (pbuf) and the column that becomes the
+// next pivot column (k+2), published by its owner during the pass.
+// Same arithmetic, in the same order, as k_sytrd_rows (bitwise identical).
+template <int RPT, int NT, bool PROF>
+__global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, int qmax, long long* prof) {
+  long long t_[8];
+#define SM_T(ix) if constexpr (PROF) t_[ix] = clock64();
+  constexpr int NW = NT / 32;
+  cg::grid_group grid = cg::this_grid();
+  const int N = (int)a.n;
+  const int64_t n = a.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NB = gridDim.x, b = blockIdx.x;
+  double* A = a.A;
+  extern __shared__ double sm[];
+  double* cols = sm;                          // qmax x N, column q = jb + NB q
+  double* part = cols + (size_t)qmax * N;     // NW x qmax per-warp partial dots
+  double* red = part + NW * qmax;             // 2 x NW
+  double* vo = red + 2 * NW;                  // qmax: v_k at the owned column indices
+  double* wo = vo + qmax;                     // qmax: w_k at the owned column indices
+  double* piv = wo + qmax;                    // [0] = v_k[k+2]
+  int rph = 0;
+  const int jb = b >= 1 ? b : b + NB;         // column 0 is only read (reflector 0)
+  const int nown = jb < N ? (N - 1 - jb) / NB + 1 : 0;
+  int qi[RPT];                                // slot of row i if i is an owned column index
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int i = tid + NT * u;
+    qi[u] = (i >= jb && i < N && (i - jb) % NB == 0) ? (i - jb) / NB : -1;
+  }
+  for (int q = 0; q < nown; ++q) {
+    const double* src = A + n * (jb + (int64_t)NB * q);
+    for (int i = tid; i < N; i += NT) cols[q * N + i] = src[i];
+  }
+
+  double vr[RPT], wr[RPT], nr[RPT];
+  double x0[RPT];
+  double s2 = 0.0, alpha = 0.0;
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int i = tid + NT * u;
+    x0[u] = (i >= 1 && i < N) ? A[i] : 0.0;
+    if (i >= 2 && i < N) s2 = fma(x0[u], x0[u], s2);
+  }
+  alpha = A[1];
+  double xn2 = bsum<NW>(s2, red, rph);
+  double tau_k = 0.0, beta = alpha, scale = 0.0;
+  if (xn2 > 0.0) {
+    const double nrm = sqrt(alpha * alpha + xn2);
+    beta = alpha >= 0.0 ? -nrm : nrm;
+    tau_k = (beta - alpha) / beta;
+    scale = 1.0 / (alpha - beta);
+  }
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int i = tid + NT * u;
+    vr[u] = i == 1 ? 1.0 : (i >= 2 && i < N ? x0[u] * scale : 0.0);
+    if (qi[u] >= 0) vo[qi[u]] = vr[u];
+    if (i == 2) piv[0] = vr[u];
+  }
+  if (b == 0) {
+    if (tid == 0) { a.d[0] = A[0]; a.e[0] = beta; a.tau[0] = tau_k; }
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int i = tid + NT * u;
+      if (i < N) a.hv[i] = vr[u];
+    }
+  }
+  __syncthreads();
+  // p_0 = tau_0 A v_0 on owned columns (no update yet)
+  for (int q = 0; q < nown; ++q) {
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int i = tid + NT * u;
+      const double cv = (i >= 1 && i < N) ? cols[q * N + i] : 0.0;
+      acc = fma(cv, vr[u], acc);
+    }
+    acc = wsum(acc);
+    if (lane == 0) part[warp * qmax + q] = acc;
+  }
+  __syncthreads();
+  if (tid < nown) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += part[w * qmax + tid];
+    a.pbuf[jb + (int64_t)NB * tid] = tau_k * s;
+  }
+  grid.sync();
+
+  int64_t k = 0;
+  for (; k + 2 < n && k < a.k_end; ++k) {
+    SM_T(0);
+    const int buf = (int)(k & 1);
+    const double* pb = a.pbuf + buf * n;
+    const int c1 = (int)k + 1;
+    double pp[RPT], xa[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int i = tid + NT * u;
+      const bool live = i >= c1 && i < N;
+      pp[u] = live ? pb[i] : 0.0;
+      xa[u] = live ? A[i + n * c1] : 0.0;
+    }
+    const double p_c1 = pb[c1], p_k2 = pb[k + 2], a_k2 = A[(k + 2) + n * c1];
+    double pv = 0.0;
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) pv = fma(pp[u], vr[u], pv);
+    SM_T(1);
+    const double K = 0.5 * tau_k * bsum<NW>(pv, red, rph);
+    SM_T(2);
+    const double v_c1 = 1.0, v_k2 = piv[0];  // v_k[k+1] = 1 by construction
+    const double w_c1 = p_c1 - K * v_c1, w_k2 = p_k2 - K * v_k2;
+    s2 = 0.0;
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int i = tid + NT * u;
+      wr[u] = pp[u] - K * vr[u];
+      xa[u] = xa[u] - vr[u] * w_c1 - wr[u] * v_c1;
+      if (i >= k + 3 && i < N) s2 = fma(xa[u], xa[u], s2);
+    }
+    if (k + 3 == n) {
+      if (b == 0) {
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+          const int i = tid + NT * u;
+          if (i == N - 2) a.d[N - 2] = xa[u];
+          if (i == N - 1) {
+            a.e[N - 2] = xa[u];
+            a.d[N - 1] = A[(n - 1) + n * (n - 1)] - 2.0 * vr[u] * wr[u];
+            a.tau[N - 2] = 0.0;
+          }
+        }
+      }
+      break;
+    }
+    xn2 = bsum<NW>(s2, red, rph);
+    alpha = a_k2 - v_k2 * w_c1 - w_k2 * v_c1;
+    double tau_n = 0.0;
+    beta = alpha;
+    scale = 0.0;
+    if (xn2 > 0.0) {
+      const double nrm = sqrt(alpha * alpha + xn2);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau_n = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int i = tid + NT * u;
+      nr[u] = i == k + 2 ? 1.0 : (i >= k + 3 && i < N ? xa[u] * scale : 0.0);
+      if (qi[u] >= 0) wo[qi[u]] = wr[u];
+    }
+    if (b == 0) {
+      if (tid == 0) { a.e[c1] = beta; a.tau[c1] = tau_n; }
+      double* h = a.hv + n * c1;
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int i = tid + NT * u;
+        if (i < N) h[i] = nr[u];
+        if (i == c1) a.d[c1] = xa[u];
+      }
+    }
+    __syncthreads();  // wo ready
+    SM_T(3);
+    double* pbn = a.pbuf + (buf ^ 1) * n;
+    const int k2 = (int)k + 2;
+    const int q0 = k2 > jb ? (k2 - jb + NB - 1) / NB : 0;
+    // Owned live columns, four per iteration: the loads/updates of the four
+    // interleave, and their four warp dot products are reduced together with a
+    // butterfly reduce-scatter (6 shuffles instead of 20). Shuffles share the
+    // MIO pipe with the shared-memory traffic that bounds this pass.
+    bool lv[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) lv[u] = tid + NT * u >= k2 && tid + NT * u < N;
+    const int qpub = (k2 - jb) % NB == 0 && k2 >= jb ? (k2 - jb) / NB : -1;
+    const int qlast = (k2 + 2 == N && (N - 1 - jb) % NB == 0 && N - 1 >= jb) ? (N - 1 - jb) / NB : -1;
+    for (int q = q0; q < nown; q += 4) {
+      double acc[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        acc[c] = 0.0;
+        if (q + c < nown) {
+          const double vj = vo[q + c], wj = wo[q + c];
+          double* cq = cols + (q + c) * N + tid;
+#pragma unroll
+          for (int u = 0; u < RPT; ++u) {
+            if (lv[u]) {
+              const double xv = cq[NT * u] - vr[u] * wj - wr[u] * vj;
+              cq[NT * u] = xv;
+              acc[c] = fma(xv, nr[u], acc[c]);
+            }
+          }
+        }
+      }
+      const bool up = lane & 16, up2 = lane & 8;
+      const double r0 = (up ? acc[2] : acc[0]) + __shfl_xor_sync(0xffffffffu, up ? acc[0] : acc[2], 16);
+      const double r1 = (up ? acc[3] : acc[1]) + __shfl_xor_sync(0xffffffffu, up ? acc[1] : acc[3], 16);
+      double t = (up2 ? r1 : r0) + __shfl_xor_sync(0xffffffffu, up2 ? r0 : r1, 8);
+      t += __shfl_xor_sync(0xffffffffu, t, 4);
+      t += __shfl_xor_sync(0xffffffffu, t, 2);
+      t += __shfl_xor_sync(0xffffffffu, t, 1);
+      const int cs = (up ? 2 : 0) + (up2 ? 1 : 0);  // column slot this lane's sum belongs to
+      if ((lane & 7) == 0 && q + cs < nown) part[warp * qmax + q + cs] = t;
+    }
+    // publish the next pivot column (and, before the last step, the last diagonal)
+    if (qpub >= q0 && qpub >= 0 && qpub < nown) {
+      double* gq = A + n * k2;
+#pragma unroll
+      for (int u = 0; u < RPT; ++u)
+        if (lv[u]) gq[tid + NT * u] = cols[qpub * N + tid + NT * u];
+    }
+    if (qlast >= 0 && qlast < nown && tid == (N - 1) % NT) A[(n - 1) + n * (n - 1)] = cols[qlast * N + N - 1];
+    SM_T(4);
+    __syncthreads();
+    SM_T(5);
+    if (tid >= q0 && tid < nown) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += part[w * qmax + tid];
+      pbn[jb + (int64_t)NB * tid] = tau_n * s;
+    }
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int i = tid + NT * u;
+      vr[u] = nr[u];
+      if (qi[u] >= 0) vo[qi[u]] = nr[u];
+      if (i == k + 3) piv[0] = nr[u];
+    }
+    tau_k = tau_n;
+    SM_T(6);
+    grid.sync();
+    if (PROF && tid == 0 && (b == 0 || b == NB / 2)) {
+      SM_T(7);
+      long long* r = prof + ((b ? 1 : 0) * 4 + (int)(4 * k / n)) * 8;
+      for (int ph = 0; ph < 7; ++ph) atomicAdd((unsigned long long*)(r + ph), (unsigned long long)(t_[ph + 1] - t_[ph]));
+      atomicAdd((unsigned long long*)(r + 7), 1ull);
+    }
+  }
+#undef SM_T
+  if (k + 2 < n) {  // stopped at k_end: the trailing block continues elsewhere from global memory
+    for (int q = 0; q < nown; ++q) {
+      double* dst = A + n * (jb + (int64_t)NB * q);
+      for (int i = tid; i < N; i += NT) dst[i] = cols[q * N + i];
+    }
+  }
+}
+
 struct RowsInfo { int blocks = 0; int64_t n = -1; };
 
 }  // namespace
+
+// Shared-memory-resident launch; false if the owned columns do not fit.
+bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* e, double* tau, double* hv,
+                double* pbuf) {
+  static const int nt_env = [] {
+    const char* s = std::getenv("TMB_SMEM_NT");  // A/B: 256 (2 blocks/SM) or 512 (1 block/SM)
+    return s ? std::atoi(s) : 0;
+  }();
+  static const int bps_env = [] {
+    const char* s = std::getenv("TMB_SMEM_BPS");  // A/B: blocks per SM
+    return s ? std::atoi(s) : 0;
+  }();
+  const int nt = nt_env ? nt_env : 512;
+  const int bps = bps_env ? bps_env : (nt == 256 ? 2 : 1);
+  const int nb = bps * c.num_sms;
+  const int rpt = (int)ceil_div(n, nt);
+  using KFn = void (*)(RowArgs, int, long long*);
+  KFn kern = nullptr;
+  int slot = 0;
+  const int qmax = (int)ceil_div(n - 1, nb);
+  static const bool prof_on = std::getenv("TMB_TRD_PROFILE") != nullptr;
+#define SMEM_K(R, T) (prof_on ? k_sytrd_smem<R, T, true> : k_sytrd_smem<R, T, false>)
+  if (nt == 512) {
+    if (rpt <= 2) { kern = SMEM_K(2, 512); slot = 0; }
+    else if (rpt <= 4) { kern = SMEM_K(4, 512); slot = 1; }
+  } else {
+    if (rpt <= 4) { kern = SMEM_K(4, 256); slot = 2; }
+    else if (rpt <= 8) { kern = SMEM_K(8, 256); slot = 3; }
+  }
+#undef SMEM_K
+  if (!kern) return false;
+  const int nw = nt / 32;
+  const size_t smem = sizeof(double) * ((size_t)qmax * n + (size_t)nw * qmax + 2 * nw + 2 * qmax + 1);
+  if (smem > 227 * 1024) return false;
+  static int64_t checked[4] = {-1, -1, -1, -1};
+  if (checked[slot] != n) {
+    TMB_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::max<size_t>(smem, 48 * 1024)));
+    int per_sm = 0;
+    TMB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kern, nt, smem));
+    if (per_sm < bps) return false;
+    checked[slot] = n;
+  }
+  // TMB_TRD_PROFILE: per-phase clock64 sums (blocks 0 and NB/2, by quarter of the reduction)
+  long long* prof = nullptr;
+  if (prof_on) {
+    prof = alloc<long long>(c, 64);
+    TMB_CUDA(cudaMemsetAsync(prof, 0, sizeof(long long) * 64, c.stream));
+  }
+  RowArgs ra{A, n, k_end, d, e, tau, hv, pbuf};
+  void* args[] = {&ra, (void*)&qmax, &prof};
+  TMB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, nb, nt, args, smem, c.stream));
+  c.launches++;
+  check_launch("k_sytrd_smem");
+  if (prof) {
+    long long h[64];
+    TMB_CUDA(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    TMB_CUDA(cudaStreamSynchronize(c.stream));
+    for (int blk = 0; blk < 2; ++blk)
+      for (int qtr = 0; qtr < 4; ++qtr) {
+        const long long* r = h + (blk * 4 + qtr) * 8;
+        if (!r[7]) continue;
+        std::fprintf(stderr, "sytrd_smem n=%lld blk %d q%d cycles/step: gather %lld K %lld house %lld pass %lld "
+                     "bar %lld pwrite %lld gridsync %lld\n", (long long)n, blk, qtr, r[0] / r[7], r[1] / r[7],
+                     r[2] / r[7], r[3] / r[7], r[4] / r[7], r[5] / r[7], r[6] / r[7]);
+      }
+  }
+  return true;
+}
 
 // Returns false when n is outside the row-partitioned kernel's range (the
 // caller then uses the column-per-warp kernel).
 bool sytrd_rows(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* e, double* tau, double* hv,
                 double* pbuf) {
   if (n > 2048 || n < 3) return false;  // rows per thread <= 8 (256 threads) / 4 (512 threads)
+  static const bool smem_off = std::getenv("TMB_SYTRD_L2") != nullptr;  // A/B: force the L2-streaming variant
+  // measured (scripts/ab_smem.sh): n=1920 8.8 vs 11.9 ms, n=1080 4.4 vs 5.0 ms,
+  // n=500 1.75 vs 1.65 ms (L2 variant keeps small n)
+  if (!smem_off && n > 600 && sytrd_smem(c, A, n, k_end, d, e, tau, hv, pbuf)) return true;
   static const int cb_env = [] {
     const char* s = std::getenv("TMB_ROWS_CB");  // A/B: columns per load batch
     return s ? std::atoi(s) : 0;

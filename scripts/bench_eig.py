@@ -30,4 +30,17 @@ for n, k in sizes:
         e.record()
         torch.cuda.synchronize()
         times.append(s.elapsed_time(e))
-    print(f"n={n} k={k}: " + " ".join(f"{t:.2f}" for t in times) + " ms")
+    import hashlib
+    digest = hashlib.sha1(vecs.cpu().numpy().tobytes() + vals.cpu().numpy().tobytes()).hexdigest()[:12]
+    w = np.linalg.eigvalsh(g)[::-1][:k]
+    err = np.abs(vals.cpu().numpy() - w).max() / w[0]
+    L.check(L.LIB.tmb_timing(h, 1), h)
+    L.check(L.LIB.tmb_leading_eigvecs(h, L.ptr(gd), n, k, L.ptr(vecs), L.ptr(vals)), h)
+    torch.cuda.synchronize()
+    fam = []
+    for tag, nm in ((1, "sytrd"), (2, "tridiag"), (4, "wy_gemm")):
+        cnt, tms, work = L.C.c_int64(), L.C.c_double(), L.C.c_double()
+        L.check(L.LIB.tmb_timing_read(h, tag, L.C.byref(cnt), L.C.byref(tms), L.C.byref(work)), h)
+        fam.append(f"{nm} {tms.value:.2f}")
+    L.check(L.LIB.tmb_timing(h, 0), h)
+    print(f"n={n} k={k}: [" + ", ".join(fam) + "] " + " ".join(f"{t:.2f}" for t in times) + f" ms  sha1 {digest}  val err {err:.1e}")

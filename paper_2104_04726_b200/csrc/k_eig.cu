@@ -425,22 +425,39 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) k_sytrd(const TrdArgs a) {
 }
 
 // ------------------------------------------------------------------ bisection
-__device__ __forceinline__ int sturm_count(const double* __restrict__ d, const double* __restrict__ e,
-                                           int64_t n, double x, double pivmin) {
-  double q = d[0] - x;
-  if (fabs(q) <= pivmin) q = -pivmin;
-  int cnt = q < 0.0;
-  for (int64_t i = 1; i < n; ++i) {
-    const double ei = e[i - 1];
-    q = (d[i] - x) - ei * ei * frcp(q);
-    if (fabs(q) <= pivmin) q = -pivmin;
-    cnt += q < 0.0;
+// Sturm counts (number of eigenvalues < x) at P shifts at once: P independent
+// LDL^T pivot chains interleave, hiding the reciprocal's latency (the chain,
+// not throughput, bounds a count).
+template <int P>
+__device__ __forceinline__ void sturm_counts(const double* __restrict__ d, const double* __restrict__ e,
+                                             int64_t n, const double (&x)[P], double pivmin, int (&cnt)[P]) {
+  double q[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    q[p] = d[0] - x[p];
+    if (fabs(q[p]) <= pivmin) q[p] = -pivmin;
+    cnt[p] = q[p] < 0.0;
   }
-  return cnt;
+  for (int64_t i = 1; i < n; ++i) {
+    const double ei = e[i - 1], di = d[i];
+    const double e2 = ei * ei;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      q[p] = (di - x[p]) - e2 * frcp(q[p]);
+      if (fabs(q[p]) <= pivmin) q[p] = -pivmin;
+      cnt[p] += q[p] < 0.0;
+    }
+  }
 }
 
+// One warp per wanted eigenvalue (descending index jd): 32-way multisection
+// (one shift per lane) of the Gershgorin interval down to absolute accuracy
+// eps*||T|| (Sturm counts resolve nothing finer), ~11 rounds. Measured: 4
+// shifts per lane (128-way, ~8 rounds) is slower (1.74 vs 0.95 ms at n=1920,
+// k=480) -- the counts are then bound by reciprocal/DFMA throughput.
 __global__ void k_bisect(const double* __restrict__ d, const double* __restrict__ e, int64_t n, int64_t k,
                          double* __restrict__ vals) {
+  constexpr int P = 1, NPT = 32 * P;
   const int lane = threadIdx.x & 31;
   const int64_t jd = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (jd >= k) return;
@@ -464,119 +481,154 @@ __global__ void k_bisect(const double* __restrict__ d, const double* __restrict_
   double hi = gu + 2.0 * DBL_EPSILON * span + 2.0 * pivmin;
   for (int round = 0; round < 24; ++round) {
     const double w = hi - lo;
-    // absolute accuracy eps*||T|| (Sturm counts resolve nothing finer)
     if (w <= 2.0 * DBL_EPSILON * fmax(fabs(gl), fabs(gu)) + 4.0 * pivmin) break;
-    const double x = lo + w * (double)(lane + 1) / 33.0;
-    const int c = sturm_count(d, e, n, x, pivmin);
-    const unsigned above = __ballot_sync(0xffffffffu, c > ja);  // eigenvalue ja < x
-    const int first = above ? __ffs(above) - 1 : 32;
-    const double xf = __shfl_sync(0xffffffffu, x, first < 32 ? first : 31);
-    const double xp = __shfl_sync(0xffffffffu, x, first > 0 ? first - 1 : 0);
-    if (first == 32) lo = xf;            // all counts <= ja: eigenvalue above x_31
-    else { hi = xf; if (first > 0) lo = xp; }
+    // shift m = p*32 + lane, ascending in m
+    double x[P];
+    int c[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) x[p] = lo + w * (double)(p * 32 + lane + 1) / (double)(NPT + 1);
+    sturm_counts<P>(d, e, n, x, pivmin, c);
+    int first = NPT;  // first shift whose count exceeds ja (eigenvalue ja < x)
+#pragma unroll
+    for (int p = P - 1; p >= 0; --p) {
+      const unsigned above = __ballot_sync(0xffffffffu, c[p] > ja);
+      if (above) first = p * 32 + __ffs(above) - 1;
+    }
+    const auto shift = [&](int m) {  // x_m, held by lane m % 32 in slot m / 32
+      double v = x[0];
+#pragma unroll
+      for (int p = 1; p < P; ++p)
+        if (m / 32 == p) v = x[p];
+      return __shfl_sync(0xffffffffu, v, m % 32);
+    };
+    if (first == NPT) {
+      lo = shift(NPT - 1);  // all counts <= ja: eigenvalue above the last shift
+    } else {
+      const double xf = shift(first);
+      const double xp = shift(first > 0 ? first - 1 : 0);
+      hi = xf;
+      if (first > 0) lo = xp;
+    }
   }
   if (lane == 0) vals[jd] = 0.5 * (lo + hi);
 }
 
 // ------------------------------------------------------------------ twisted factorisation
-// z (unnormalised) for eigenvalue vals[j]; scratch dp/dm laid out [i][j] for coalescing.
+// One warp per eigenvalue: lane 0 runs the stationary (top-down) D+ chain while
+// lane 1 runs the progressive (bottom-up) D- chain; the twist index r =
+// argmin |gamma| is a warp reduction; the ratios of the two z recurrences are
+// formed by all lanes, the two products chains again by lanes 0 and 1; then
+// the column is scaled to unit norm (max-abs prescaled) straight into vecs.
+// Scratch dp/dm/z are per-eigenvalue columns of length n.
 __global__ void k_twisted(const double* __restrict__ d, const double* __restrict__ e, int64_t n, int64_t k,
                           const double* __restrict__ vals, double* __restrict__ dp, double* __restrict__ dm,
-                          double* __restrict__ zrow) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= k) return;
-  const double lam = vals[j];
-  double emax2 = 0.0;
-  for (int64_t i = 0; i + 1 < n; ++i) emax2 = fmax(emax2, e[i] * e[i]);
-  const double pivmin = DBL_MIN * fmax(1.0, emax2);
-  // stationary (top-down) D+
-  double q = d[0] - lam;
-  if (fabs(q) <= pivmin) q = -pivmin;
-  dp[j] = q;
-  for (int64_t i = 1; i < n; ++i) {
-    const double ei = e[i - 1];
-    q = (d[i] - lam) - ei * ei * frcp(q);
-    if (fabs(q) <= pivmin) q = -pivmin;
-    dp[i * k + j] = q;
-  }
-  // progressive (bottom-up) D-, twist index r = argmin |gamma|
-  double m = d[n - 1] - lam;
-  if (fabs(m) <= pivmin) m = -pivmin;
-  dm[(n - 1) * k + j] = m;
-  int64_t r = n - 1;
-  double gbest = fabs(dp[(n - 1) * k + j]);  // gamma_{n-1} = D+_{n-1}
-  for (int64_t i0 = n - 2; i0 >= 0; i0 -= 8) {
-    double dpv[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) dpv[u] = i0 - u >= 0 ? dp[(i0 - u) * k + j] : 0.0;  // prefetch
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int64_t i = i0 - u;
-      if (i < 0) break;
-      const double ei = e[i];
-      const double t = (d[i] - lam) - ei * ei * frcp(m);
-      m = fabs(t) <= pivmin ? -pivmin : t;
-      dm[i * k + j] = m;
-      const double gamma = dpv[u] + m - (d[i] - lam);
-      if (fabs(gamma) < gbest) { gbest = fabs(gamma); r = i; }
-    }
-  }
-  // z_r = 1, outward recurrences; the ratios do not depend on z, so they are
-  // computed 8 at a time ahead of the multiply chain.
-  zrow[r * k + j] = 1.0;
-  constexpr int U = 8;
-  double z = 1.0;
-  for (int64_t i0 = r - 1; i0 >= 0; i0 -= U) {
-    double rt[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = i0 - u;
-      rt[u] = i >= 0 ? -e[i] * frcp(dp[i * k + j]) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = i0 - u;
-      if (i >= 0) {
-        z = rt[u] * z;
-        if (!(fabs(z) < 1e280)) z = (z > 0 ? 1e280 : -1e280);
-        zrow[i * k + j] = z;
-      }
-    }
-  }
-  z = 1.0;
-  for (int64_t i0 = r + 1; i0 < n; i0 += U) {
-    double rt[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = i0 + u;
-      rt[u] = i < n ? -e[i - 1] * frcp(dm[i * k + j]) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = i0 + u;
-      if (i < n) {
-        z = rt[u] * z;
-        if (!(fabs(z) < 1e280)) z = (z > 0 ? 1e280 : -1e280);
-        zrow[i * k + j] = z;
-      }
-    }
-  }
-}
-
-// ------------------------------------------------------------------ back-transformation
-// z (row layout [i][j]) -> x (column-major), each column scaled to unit norm.
-__global__ void k_znorm(const double* __restrict__ zrow, int64_t n, int64_t k, double* __restrict__ x) {
+                          double* __restrict__ z, double* __restrict__ vecs) {
   const int lane = threadIdx.x & 31;
   const int64_t j = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (j >= k) return;
+  const double lam = vals[j];
+  double emax2 = 0.0;
+  for (int64_t i = lane; i + 1 < n; i += 32) emax2 = fmax(emax2, e[i] * e[i]);
+  for (int o = 16; o > 0; o >>= 1) emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
+  const double pivmin = DBL_MIN * fmax(1.0, emax2);
+  double* dpj = dp + j * n;
+  double* dmj = dm + j * n;
+  double* zj = z + j * n;
+  constexpr int U = 8;
+  if (lane == 0) {  // D+ (stationary qd, top-down)
+    double q = d[0] - lam;
+    if (fabs(q) <= pivmin) q = -pivmin;
+    dpj[0] = q;
+    for (int64_t i0 = 1; i0 < n; i0 += U) {
+      double dv[U], ev[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        dv[u] = i0 + u < n ? d[i0 + u] : 0.0;
+        ev[u] = i0 + u < n ? e[i0 + u - 1] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i0 + u >= n) break;
+        q = (dv[u] - lam) - ev[u] * ev[u] * frcp(q);
+        if (fabs(q) <= pivmin) q = -pivmin;
+        dpj[i0 + u] = q;
+      }
+    }
+  } else if (lane == 1) {  // D- (progressive qd, bottom-up)
+    double m = d[n - 1] - lam;
+    if (fabs(m) <= pivmin) m = -pivmin;
+    dmj[n - 1] = m;
+    for (int64_t i0 = n - 2; i0 >= 0; i0 -= U) {
+      double dv[U], ev[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        dv[u] = i0 - u >= 0 ? d[i0 - u] : 0.0;
+        ev[u] = i0 - u >= 0 ? e[i0 - u] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i0 - u < 0) break;
+        const double t = (dv[u] - lam) - ev[u] * ev[u] * frcp(m);
+        m = fabs(t) <= pivmin ? -pivmin : t;
+        dmj[i0 - u] = m;
+      }
+    }
+  }
+  __syncwarp();
+  // twist index: argmin |gamma_i|, ties to the larger i (gamma_{n-1} = D+_{n-1})
+  double gbest = 1e308;
+  int64_t r = -1;
+  for (int64_t i = lane; i < n; i += 32) {
+    const double g = i == n - 1 ? fabs(dpj[i]) : fabs(dpj[i] + dmj[i] - (d[i] - lam));
+    if (g < gbest || (g == gbest && i > r)) { gbest = g; r = i; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double og = __shfl_xor_sync(0xffffffffu, gbest, o);
+    const int64_t orr = __shfl_xor_sync(0xffffffffu, r, o);
+    if (og < gbest || (og == gbest && orr > r)) { gbest = og; r = orr; }
+  }
+  // ratios of z_i / z_{i+1} (i < r) and z_i / z_{i-1} (i > r)
+  for (int64_t i = lane; i < n; i += 32)
+    zj[i] = i < r ? -e[i] * frcp(dpj[i]) : (i > r ? -e[i - 1] * frcp(dmj[i]) : 1.0);
+  __syncwarp();
+  if (lane == 0) {  // z_r = 1, upward products
+    double zz = 1.0;
+    for (int64_t i0 = r - 1; i0 >= 0; i0 -= U) {
+      double rt[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) rt[u] = i0 - u >= 0 ? zj[i0 - u] : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i0 - u < 0) break;
+        zz = rt[u] * zz;
+        if (!(fabs(zz) < 1e280)) zz = (zz > 0 ? 1e280 : -1e280);
+        zj[i0 - u] = zz;
+      }
+    }
+  } else if (lane == 1) {  // downward products
+    double zz = 1.0;
+    for (int64_t i0 = r + 1; i0 < n; i0 += U) {
+      double rt[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) rt[u] = i0 + u < n ? zj[i0 + u] : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i0 + u >= n) break;
+        zz = rt[u] * zz;
+        if (!(fabs(zz) < 1e280)) zz = (zz > 0 ? 1e280 : -1e280);
+        zj[i0 + u] = zz;
+      }
+    }
+  }
+  __syncwarp();
   double mx = 0.0;
-  for (int64_t i = lane; i < n; i += 32) mx = fmax(mx, fabs(zrow[i * k + j]));
+  for (int64_t i = lane; i < n; i += 32) mx = fmax(mx, fabs(zj[i]));
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   const double inv = mx > 0.0 ? 1.0 / mx : 1.0;
   double s = 0.0;
-  for (int64_t i = lane; i < n; i += 32) { const double v = zrow[i * k + j] * inv; s = fma(v, v, s); }
+  for (int64_t i = lane; i < n; i += 32) { const double v = zj[i] * inv; s = fma(v, v, s); }
   const double nrm = inv / sqrt(warp_sum(s));
-  for (int64_t i = lane; i < n; i += 32) x[i + n * j] = zrow[i * k + j] * nrm;
+  for (int64_t i = lane; i < n; i += 32) vecs[i + n * j] = zj[i] * nrm;
 }
 
 // Compact-WY T factor of one panel of nb forward reflectors (LAPACK dlarft):
@@ -820,15 +872,13 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
   }
   double* dp = alloc<double>(c, (size_t)n * k);
   double* dm = alloc<double>(c, (size_t)n * k);
-  double* zrow = alloc<double>(c, (size_t)n * k);
+  double* zs = alloc<double>(c, (size_t)n * k);
   {
     Timed timed_tri(c, TAG_TRIDIAG, 0.0);
     k_bisect<<<(unsigned)ceil_div(k, 8), 256, 0, c.stream>>>(d, e, n, k, vals);
     LAUNCHED("k_bisect");
-    k_twisted<<<(unsigned)ceil_div(k, 128), 128, 0, c.stream>>>(d, e, n, k, vals, dp, dm, zrow);
+    k_twisted<<<(unsigned)ceil_div(k, 8), 256, 0, c.stream>>>(d, e, n, k, vals, dp, dm, zs, vecs);
     LAUNCHED("k_twisted");
-    k_znorm<<<(unsigned)ceil_div(k, 8), 256, 0, c.stream>>>(zrow, n, k, vecs);
-    LAUNCHED("k_znorm");
   }
   backtransform(c, hv, tau, n, hv_cols, k, vecs);
   orthonormalize(c, vecs, n, k);

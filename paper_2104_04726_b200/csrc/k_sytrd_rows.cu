@@ -34,6 +34,15 @@ struct RowArgs {
   double* pbuf;  // 2 x n: p_k by step parity
 };
 
+__device__ __forceinline__ double frcp(double b) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  double e = fma(-b, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-b, r, 1.0);
+  return fma(r, e, r);
+}
+
 __device__ __forceinline__ double wsum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
@@ -282,7 +291,7 @@ __global__ void __launch_bounds__(RW_THREADS, 512 / RW_THREADS) k_sytrd_rows(con
 // Same arithmetic, in the same order, as k_sytrd_rows (bitwise identical).
 template <int RPT, int NT, bool PROF>
 __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, int qmax, long long* prof) {
-  long long t_[8];
+  long long t_[10];
 #define SM_T(ix) if constexpr (PROF) t_[ix] = clock64();
   constexpr int NW = NT / 32;
   cg::grid_group grid = cg::this_grid();
@@ -414,16 +423,20 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
       break;
     }
     xn2 = bsum<NW>(s2, red, rph);
+    SM_T(3);
     alpha = a_k2 - v_k2 * w_c1 - w_k2 * v_c1;
     double tau_n = 0.0;
     beta = alpha;
     scale = 0.0;
     if (xn2 > 0.0) {
+      // reciprocals by rcp.approx + 2 Newton steps (independent, ~1 ulp)
+      // instead of two IEEE divisions on the step's serial path
       const double nrm = sqrt(alpha * alpha + xn2);
       beta = alpha >= 0.0 ? -nrm : nrm;
-      tau_n = (beta - alpha) / beta;
-      scale = 1.0 / (alpha - beta);
+      tau_n = (beta - alpha) * frcp(beta);
+      scale = frcp(alpha - beta);
     }
+    SM_T(4);
 #pragma unroll
     for (int u = 0; u < RPT; ++u) {
       const int i = tid + NT * u;
@@ -441,7 +454,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
       }
     }
     __syncthreads();  // wo ready
-    SM_T(3);
+    SM_T(5);
     double* pbn = a.pbuf + (buf ^ 1) * n;
     const int k2 = (int)k + 2;
     const int q0 = k2 > jb ? (k2 - jb + NB - 1) / NB : 0;
@@ -490,9 +503,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
         if (lv[u]) gq[tid + NT * u] = cols[qpub * N + tid + NT * u];
     }
     if (qlast >= 0 && qlast < nown && tid == (N - 1) % NT) A[(n - 1) + n * (n - 1)] = cols[qlast * N + N - 1];
-    SM_T(4);
+    SM_T(6);
     __syncthreads();
-    SM_T(5);
+    SM_T(7);
     if (tid >= q0 && tid < nown) {
       double s = 0.0;
 #pragma unroll
@@ -507,13 +520,13 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
       if (i == k + 3) piv[0] = nr[u];
     }
     tau_k = tau_n;
-    SM_T(6);
+    SM_T(8);
     grid.sync();
     if (PROF && tid == 0 && (b == 0 || b == NB / 2)) {
-      SM_T(7);
-      long long* r = prof + ((b ? 1 : 0) * 4 + (int)(4 * k / n)) * 8;
-      for (int ph = 0; ph < 7; ++ph) atomicAdd((unsigned long long*)(r + ph), (unsigned long long)(t_[ph + 1] - t_[ph]));
-      atomicAdd((unsigned long long*)(r + 7), 1ull);
+      SM_T(9);
+      long long* r = prof + ((b ? 1 : 0) * 4 + (int)(4 * k / n)) * 10;
+      for (int ph = 0; ph < 9; ++ph) atomicAdd((unsigned long long*)(r + ph), (unsigned long long)(t_[ph + 1] - t_[ph]));
+      atomicAdd((unsigned long long*)(r + 9), 1ull);
     }
   }
 #undef SM_T
@@ -574,8 +587,8 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
   // TMB_TRD_PROFILE: per-phase clock64 sums (blocks 0 and NB/2, by quarter of the reduction)
   long long* prof = nullptr;
   if (prof_on) {
-    prof = alloc<long long>(c, 64);
-    TMB_CUDA(cudaMemsetAsync(prof, 0, sizeof(long long) * 64, c.stream));
+    prof = alloc<long long>(c, 80);
+    TMB_CUDA(cudaMemsetAsync(prof, 0, sizeof(long long) * 80, c.stream));
   }
   RowArgs ra{A, n, k_end, d, e, tau, hv, pbuf};
   void* args[] = {&ra, (void*)&qmax, &prof};
@@ -583,16 +596,17 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
   c.launches++;
   check_launch("k_sytrd_smem");
   if (prof) {
-    long long h[64];
+    long long h[80];
     TMB_CUDA(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
     TMB_CUDA(cudaStreamSynchronize(c.stream));
     for (int blk = 0; blk < 2; ++blk)
       for (int qtr = 0; qtr < 4; ++qtr) {
-        const long long* r = h + (blk * 4 + qtr) * 8;
-        if (!r[7]) continue;
-        std::fprintf(stderr, "sytrd_smem n=%lld blk %d q%d cycles/step: gather %lld K %lld house %lld pass %lld "
-                     "bar %lld pwrite %lld gridsync %lld\n", (long long)n, blk, qtr, r[0] / r[7], r[1] / r[7],
-                     r[2] / r[7], r[3] / r[7], r[4] / r[7], r[5] / r[7], r[6] / r[7]);
+        const long long* r = h + (blk * 4 + qtr) * 10;
+        if (!r[9]) continue;
+        const long long m = r[9];
+        std::fprintf(stderr, "sytrd_smem n=%lld blk %d q%d cycles/step: gather %lld K %lld xn2 %lld housemath %lld "
+                     "nr+wo+bar %lld pass %lld bar %lld pwrite %lld gridsync %lld\n", (long long)n, blk, qtr,
+                     r[0] / m, r[1] / m, r[2] / m, r[3] / m, r[4] / m, r[5] / m, r[6] / m, r[7] / m, r[8] / m);
       }
   }
   return true;

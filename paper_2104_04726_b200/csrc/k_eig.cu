@@ -718,6 +718,168 @@ static int wy_nb() {
   return v;
 }
 
+// ------------------------------------------------------------------ fused compact-WY application
+// x <- x - (V_p T_p)(V_p^T x) for every 64-reflector panel p (last first), in
+// ONE launch: CTA b keeps its CB columns of x resident in shared memory and
+// streams V_p / VT_p = V_p T_p through an ST-deep ring of 64-row staging tiles
+// (L2 latency is the bound: ~100 KB in flight per SM); both products run on
+// DMMA (m16n8k8 f64, N padded to 8). Columns of x are independent, so there is
+// no inter-CTA communication (the per-panel GEMM + split-K pairs it replaces
+// were latency-bound: 90 small launches at n=1920).
+namespace wy {
+constexpr int NB = 64, NT = 256, LDW = NB + 4;
+__device__ __forceinline__ void mma(double (&c)[4], const double (&a)[4], const double (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+template <int BYTES>
+__device__ __forceinline__ void cpa(double* dst, const double* src, int bytes) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(src), "r"(bytes));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(bytes));
+}
+}  // namespace wy
+
+// CB: columns of x per CTA (<= 8, MMA N padded to 8); RC: rows per staged
+// chunk (8 warps x 16 rows in the update, 2 x RC/2 rows in the W product);
+// ST: staging ring depth.
+template <int CB, int RC, int ST>
+__global__ void __launch_bounds__(wy::NT, 1)
+    k_apply_wy(const double* __restrict__ hv, const double* __restrict__ VT, int64_t n, int64_t k, int np,
+               int ldx, int vec, double* __restrict__ x) {
+  using namespace wy;
+  constexpr int LDS_ = RC + 4;
+  static_assert(RC == 128, "update phase maps 8 warps x 16 rows");
+  extern __shared__ __align__(16) double smw[];
+  double* stg = smw;                          // ST x (NB x LDS_) staging [jj][row]
+  double* Xs = stg + ST * NB * LDS_;          // CB x ldx, column c at Xs + c*ldx
+  double* Ws = Xs + (size_t)CB * ldx;         // 8 x LDW: W[jj][c] at Ws[c*LDW + jj] (c >= CB stay 0)
+  double* scr = Ws + 8 * LDW;                 // 4 warps x 32 lanes x 4 partials
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tig = lane & 3, mt = warp & 3, kh = warp >> 2;
+  const int64_t j0 = (int64_t)blockIdx.x * CB;
+  const int N = (int)n;
+  for (int e = tid; e < CB * ldx; e += NT) {
+    const int c = e / ldx, i = e % ldx;
+    Xs[e] = (i < N && j0 + c < k) ? x[i + n * (j0 + c)] : 0.0;
+  }
+  for (int e = tid; e < 8 * LDW; e += NT) Ws[e] = 0.0;
+  // chunk cursor: panel p (descending), phase 0 = V_p rows, 1 = VT_p rows, row r
+  struct Cur { int p, ph, r; };
+  auto advance = [&](Cur& q) {
+    q.r += RC;
+    if (q.r >= N) {
+      if (q.ph == 0) { q.ph = 1; q.r = q.p * NB; }
+      else { --q.p; q.ph = 0; q.r = q.p >= 0 ? q.p * NB : 0; }
+    }
+  };
+  auto load = [&](const Cur& q, int st) {
+    if (q.p < 0) return;
+    const double* src = (q.ph == 0 ? hv : VT) + n * (int64_t)q.p * NB;
+    double* dst = stg + st * NB * LDS_;
+    if (vec) {
+#pragma unroll
+      for (int u = 0; u < NB * RC / 2 / NT; ++u) {
+        const int e = tid + NT * u, il = (e % (RC / 2)) * 2, jj = e / (RC / 2);
+        const int i = q.r + il;
+        const int nbytes = i + 1 < N ? 16 : (i < N ? 8 : 0);
+        wy::cpa<16>(dst + jj * LDS_ + il, nbytes ? src + i + n * jj : src, nbytes);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < NB * RC / NT; ++u) {
+        const int e = tid + NT * u, il = e % RC, jj = e / RC;
+        const int i = q.r + il;
+        wy::cpa<8>(dst + jj * LDS_ + il, i < N ? src + i + n * jj : src, i < N ? 8 : 0);
+      }
+    }
+  };
+  Cur cu{np - 1, 0, (np - 1) * NB};
+  Cur ld = cu;
+#pragma unroll
+  for (int s = 0; s < ST - 1; ++s) {
+    load(ld, s);
+    asm volatile("cp.async.commit_group;\n" ::);
+    advance(ld);
+  }
+  int st = 0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  while (cu.p >= 0) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(ST - 2));
+    __syncthreads();  // chunk `st` landed; the stage refilled below was released last iteration
+    load(ld, st == 0 ? ST - 1 : st - 1);
+    asm volatile("cp.async.commit_group;\n" ::);
+    advance(ld);
+    const double* sb = stg + st * NB * LDS_;
+    if (cu.ph == 0) {  // W partial += V_chunk^T X_chunk  (m = jj: warp mt; k = rows: half kh)
+#pragma unroll
+      for (int kk = 0; kk < RC / 2; kk += 8) {
+        const int kr = kh * (RC / 2) + kk;
+        const int m0 = mt * 16 + g;
+        double a[4], b[2];
+        a[0] = sb[m0 * LDS_ + kr + tig];
+        a[1] = sb[(m0 + 8) * LDS_ + kr + tig];
+        a[2] = sb[m0 * LDS_ + kr + tig + 4];
+        a[3] = sb[(m0 + 8) * LDS_ + kr + tig + 4];
+        b[0] = g < CB ? Xs[g * ldx + cu.r + kr + tig] : 0.0;
+        b[1] = g < CB ? Xs[g * ldx + cu.r + kr + tig + 4] : 0.0;
+        mma(acc, a, b);
+      }
+    } else {  // X_chunk -= VT_chunk W  (m = rows: warp's 16; k = jj)
+      double o[4] = {0.0, 0.0, 0.0, 0.0};
+      const int m0 = warp * 16 + g;
+#pragma unroll
+      for (int kb = 0; kb < NB; kb += 8) {
+        double a[4], b[2];
+        a[0] = sb[(kb + tig) * LDS_ + m0];
+        a[1] = sb[(kb + tig) * LDS_ + m0 + 8];
+        a[2] = sb[(kb + tig + 4) * LDS_ + m0];
+        a[3] = sb[(kb + tig + 4) * LDS_ + m0 + 8];
+        b[0] = Ws[g * LDW + kb + tig];
+        b[1] = Ws[g * LDW + kb + tig + 4];
+        mma(o, a, b);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = cu.r + m0 + ((r & 2) ? 8 : 0), c = 2 * tig + (r & 1);
+        if (i < N && c < CB) Xs[c * ldx + i] -= o[r];
+      }
+    }
+    Cur nx = cu;
+    advance(nx);
+    if (cu.ph == 0 && nx.ph == 1) {  // W complete: combine the two row halves into Ws
+      if (kh == 1) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) scr[(mt * 32 + lane) * 4 + r] = acc[r];
+      }
+      __syncthreads();
+      if (kh == 0) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int jj = mt * 16 + g + ((r & 2) ? 8 : 0), c = 2 * tig + (r & 1);
+          if (c < CB) Ws[c * LDW + jj] = acc[r] + scr[(mt * 32 + lane) * 4 + r];
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] = 0.0;
+    }
+    __syncthreads();  // stage st and Ws free for reuse
+    cu = nx;
+    st = st + 1 == ST ? 0 : st + 1;
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  for (int e = tid; e < CB * ldx; e += NT) {
+    const int c = e / ldx, i = e % ldx;
+    if (i < N && j0 + c < k) x[i + n * (j0 + c)] = Xs[e];
+  }
+}
+
 // x <- H_0 H_1 ... H_{n-3} x by compact-WY panels of WY_NB reflectors, last
 // panel first: x <- x - (V_p T_p) (V_p^T x). hv is n x hv_cols with zero
 // columns past the last reflector; tau is zero-padded likewise.
@@ -756,18 +918,41 @@ static void backtransform(Ctx& c, const double* hv, const double* tau, int64_t n
     g.C = VT; g.sCm = 1; g.sCn = n; g.sCb = n * nb;
     gemm(c, g);
   }
+  constexpr int CB = 4, RC = 128, ST = 2;
+  const int ldx = (int)(ceil_div(n, RC) * RC + 4);
+  const size_t fsmem =
+      sizeof(double) * ((size_t)ST * wy::NB * (RC + 4) + (size_t)CB * ldx + 8 * wy::LDW + 4 * 32 * 4);
+  static const bool fused_off = std::getenv("TMB_WY_GEMMS") != nullptr;  // A/B: per-panel GEMM path
+  if (!fused_off && nb == wy::NB && fsmem <= 227 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      TMB_CUDA(cudaFuncSetAttribute(k_apply_wy<CB, RC, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      attr = true;
+    }
+    const int vec = (n % 2 == 0 && reinterpret_cast<uintptr_t>(hv) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(VT) % 16 == 0) ? 1 : 0;
+    Timed timed(c, TAG_EIG_GEMM, 4.0 * (double)n * n * k / 2);
+    k_apply_wy<CB, RC, ST><<<(unsigned)ceil_div(k, CB), wy::NT, fsmem, c.stream>>>(hv, VT, n, k, np, ldx, vec, x);
+    LAUNCHED("k_apply_wy");
+    c.arena.release(mk);
+    return;
+  }
   for (int p = np - 1; p >= 0; --p) {
-    GemmDesc g;  // W = V_p^T x
-    g.M = nb; g.N = k; g.K1 = n;
-    g.A = hv + (int64_t)p * n * nb; g.sAm = n; g.sAk1 = 1;
-    g.B = x; g.sBk1 = 1; g.sBn = n;
+    // reflector j has v_j[i] = 0 for i <= j, so panel p only touches rows
+    // >= p*nb (kept a multiple of nb so the operands stay 16-byte aligned)
+    const int64_t r0 = std::min<int64_t>((int64_t)p * nb, n);
+    if (r0 >= n) continue;
+    GemmDesc g;  // W = V_p^T x (rows r0..n-1)
+    g.M = nb; g.N = k; g.K1 = n - r0;
+    g.A = hv + (int64_t)p * n * nb + r0; g.sAm = n; g.sAk1 = 1;
+    g.B = x + r0; g.sBk1 = 1; g.sBn = n;
     g.C = W; g.sCm = 1; g.sCn = nb;
     gemm(c, g);
-    GemmDesc u;  // x -= VT_p W
-    u.M = n; u.N = k; u.K1 = nb;
-    u.A = VT + (int64_t)p * n * nb; u.sAm = 1; u.sAk1 = n;
+    GemmDesc u;  // x -= VT_p W (rows r0..n-1)
+    u.M = n - r0; u.N = k; u.K1 = nb;
+    u.A = VT + (int64_t)p * n * nb + r0; u.sAm = 1; u.sAk1 = n;
     u.B = W; u.sBk1 = 1; u.sBn = nb;
-    u.C = x; u.sCm = 1; u.sCn = n;
+    u.C = x + r0; u.sCm = 1; u.sCn = n;
     u.alpha = -1.0; u.beta = 1.0;
     gemm(c, u);
   }

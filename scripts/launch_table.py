@@ -6,6 +6,8 @@ import sys
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
 h, data = rows[0], rows[1:]
 ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+mi = h.index("Metric Name")
+data = [r for r in data if r[mi] == "gpu__time_duration.sum"]
 agg = collections.OrderedDict()
 for r in data:
     name = r[ki].split("(")[0].split("<")[0][-40:]

@@ -133,6 +133,29 @@ def test_eig_graded_spectrum_large():
     assert np.abs(w - wr).max() / wr[0] < 1e-13
 
 
+@pytest.mark.parametrize("n,k", [(601, 1), (1023, 255), (1537, 401), (1920, 480), (1999, 3), (2048, 512),
+                                 (2101, 97)])
+def test_eig_kernel_paths_vs_lapack(n, k):
+    """Every tridiagonalisation/back-transform variant boundary: shared-memory
+    rows kernel (601..1999, odd n -> unaligned WY streaming, ragged k -> partial
+    column blocks), L2 rows kernel (2048), column kernel (2101)."""
+    rng = np.random.default_rng(n + k)
+    q = rand_orth(rng, n, n)
+    lam = 1e3 * np.exp(-np.linspace(0, 18, n))
+    g = (q * lam) @ q.T
+    g = 0.5 * (g + g.T)
+    v, w = tb.leading_eigvecs(g, k)
+    vr, wr = oracle.leading_eigvecs(g, k)
+    from conftest import principal_angle
+
+    assert np.abs(v.T @ v - np.eye(k)).max() < 1e-12
+    assert np.abs(w - wr).max() / wr[0] < 1e-13
+    assert np.abs(g @ v - v * w).max() / wr[0] < 1e-12
+    assert principal_angle(v, vr) < 1e-8
+    v2, w2 = tb.leading_eigvecs(g, k)
+    assert np.array_equal(v, v2) and np.array_equal(w, w2)  # deterministic
+
+
 def test_eig_deterministic():  # tests/test_tensor.py:218-223
     rng = np.random.default_rng(9)
     b = rng.standard_normal((300, 300))

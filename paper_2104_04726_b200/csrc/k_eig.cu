@@ -454,7 +454,9 @@ __device__ __forceinline__ void sturm_counts(const double* __restrict__ d, const
 // (one shift per lane) of the Gershgorin interval down to absolute accuracy
 // eps*||T|| (Sturm counts resolve nothing finer), ~11 rounds. Measured: 4
 // shifts per lane (128-way, ~8 rounds) is slower (1.74 vs 0.95 ms at n=1920,
-// k=480) -- the counts are then bound by reciprocal/DFMA throughput.
+// k=480) -- the counts are then bound by reciprocal/DFMA throughput -- and so
+// is the division-free three-term (p_i) recurrence with power-of-two
+// renormalisation (2.0 vs 1.2 ms incl. vectors): the LDL^T chain is kept.
 __global__ void k_bisect(const double* __restrict__ d, const double* __restrict__ e, int64_t n, int64_t k,
                          double* __restrict__ vals) {
   constexpr int P = 1, NPT = 32 * P;
@@ -1060,9 +1062,11 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
   double* zs = alloc<double>(c, (size_t)n * k);
   {
     Timed timed_tri(c, TAG_TRIDIAG, 0.0);
-    k_bisect<<<(unsigned)ceil_div(k, 8), 256, 0, c.stream>>>(d, e, n, k, vals);
+    // 2 warps (eigenvalues) per block: the counts are FP64-throughput bound, so
+    // spread the k warps over all SMs (k/8 blocks of 8 warps left 60 % idle)
+    k_bisect<<<(unsigned)ceil_div(k, 2), 64, 0, c.stream>>>(d, e, n, k, vals);
     LAUNCHED("k_bisect");
-    k_twisted<<<(unsigned)ceil_div(k, 8), 256, 0, c.stream>>>(d, e, n, k, vals, dp, dm, zs, vecs);
+    k_twisted<<<(unsigned)ceil_div(k, 2), 64, 0, c.stream>>>(d, e, n, k, vals, dp, dm, zs, vecs);
     LAUNCHED("k_twisted");
   }
   backtransform(c, hv, tau, n, hv_cols, k, vecs);

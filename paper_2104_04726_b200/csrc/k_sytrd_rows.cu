@@ -555,7 +555,11 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
   }();
   const int nt = nt_env ? nt_env : 512;
   const int bps = bps_env ? bps_env : (nt == 256 ? 2 : 1);
-  const int nb = bps * c.num_sms;
+  static const int nb_env = [] {
+    const char* s = std::getenv("TMB_SMEM_NB");  // A/B: grid size (blocks)
+    return s ? std::atoi(s) : 0;
+  }();
+  const int nb = nb_env > 0 ? std::min(nb_env, bps * c.num_sms) : bps * c.num_sms;
   const int rpt = (int)ceil_div(n, nt);
   using KFn = void (*)(RowArgs, int, long long*);
   KFn kern = nullptr;

@@ -65,6 +65,36 @@ def test_c2_full_size_properties():
     assert np.abs(a.levels).max() == 1024  # 10-bit at qp 39: max|level| = 2^10
 
 
+def _properties(cfg, sweeps, res):
+    res.model.validate()
+    fits = [r.fit for r in res.trace.records]
+    assert len(fits) == sweeps + 1
+    assert all(y >= x - 1e-12 for x, y in zip(fits, fits[1:]))
+    assert abs((1.0 - res.rel_err) - fits[-1]) < 1e-6
+    core = res.model.core.array
+    assert np.abs(core - res.levels * res.step).max() <= res.step / 2 * (1 + 1e-12)
+
+
+def test_c3_full_size_properties():
+    """BASELINE config 3 (one 1080p frame, Y'CbCr, ranks (135,240,3,5), 8-bit)."""
+    cfg = CONFIGS["c3"]
+    images = make_stack(cfg, seed=3)
+    res = tb.encode_stack(images, cfg.space, cfg.ranks, cfg.sweeps, cfg.qp)
+    _properties(cfg, cfg.sweeps, res)
+    assert np.abs(res.levels).max() == 256  # 8-bit at qp 51
+
+
+def test_c4_large_modes_properties():
+    """BASELINE config 4 at its largest ranks (2160x3840x3x14, ranks (1080,1920,3,7)):
+    Grams of n = 2160 and 3840 take the column-kernel tridiagonalisation and
+    the unfused back-transform; 2 sweeps, unquantised-curve point (qp 51)."""
+    cfg = CONFIGS["c4_2"]
+    images = make_stack(cfg, seed=4)
+    res = tb.encode_stack(images, cfg.space, cfg.ranks, 2, 51)
+    _properties(cfg, 2, res)
+    assert 0.9 < res.trace.records[-1].fit < 1.0
+
+
 def test_c1_full_config_exact_k():
     """BASELINE config 1 (the CPU-runnable case) against its golden, via the
     f64 drop-in API on the same fp32-rounded tensor the golden used."""

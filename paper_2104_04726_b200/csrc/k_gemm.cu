@@ -21,9 +21,14 @@ namespace tmb {
 namespace {
 
 #ifndef TMB_GEMM_ST
-#define TMB_GEMM_ST 3
+#define TMB_GEMM_ST 4
 #endif
-constexpr int BM = 128, BN = 64, BK = 16, ST = TMB_GEMM_ST, NT = 256;
+#ifndef TMB_GEMM_BM
+#define TMB_GEMM_BM 64
+#endif
+// CTA tile BM x 64 x 16; warps of 32x32 (BM/32 along M, 2 along N)
+constexpr int BM = TMB_GEMM_BM, BN = 64, BK = 16, ST = TMB_GEMM_ST, WMW = BM / 32, NT = 32 * WMW * (BN / 32);
+constexpr int MINB = 512 / NT;  // resident CTAs per SM the register budget is sized for
 
 template <typename T> struct Pad;
 template <> struct Pad<double> { static constexpr int v = 4; };  // 132 = 4 mod 16 (8B banks)
@@ -116,7 +121,7 @@ struct Plan {
 };
 
 template <typename TA, typename TB, bool AMF, bool BNF>
-__global__ void __launch_bounds__(NT, 2) k_gemm_dmma(const KArgs p) {
+__global__ void __launch_bounds__(NT, MINB) k_gemm_dmma(const KArgs p) {
   using TlA = Tile<TA, AMF, BM>;
   using TlB = Tile<TB, BNF, BN>;
   constexpr int VA = 16 / sizeof(TA), VB = 16 / sizeof(TB);
@@ -126,7 +131,7 @@ __global__ void __launch_bounds__(NT, 2) k_gemm_dmma(const KArgs p) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tig = lane & 3;
-  const int wm = warp & 3, wn = warp >> 2;
+  const int wm = warp % WMW, wn = warp / WMW;
   const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
   if (p.syrk && n0 + BN <= m0) return;  // tile strictly below the diagonal
   const int b = blockIdx.z % p.batch, split = blockIdx.z / p.batch;

@@ -82,28 +82,30 @@ constexpr int SG_THREADS = 256, SG_MAXPP = 9;  // K <= 64 -> 2080 pairs <= 9*256
 template <typename T>
 __global__ void __launch_bounds__(SG_THREADS) k_small_gram(const T* __restrict__ x, int64_t L, int K,
                                                            int64_t Rr, int TP, double* __restrict__ part) {
-  extern __shared__ double sX[];  // [k][TP]
+  extern __shared__ double sX[];  // [k][TP + 1]: odd row stride, so the K rows of one column sit in different banks
   __shared__ double red[SG_THREADS];
   const int npairs = K * (K + 1) / 2;
   const int G = npairs >= SG_THREADS ? 1 : SG_THREADS / npairs;
   const int tid = threadIdx.x;
   const int grp = npairs >= SG_THREADS ? 0 : tid / npairs;
   const int64_t P = L * Rr;
+  const int TPS = TP + 1;
   double acc[SG_MAXPP];
 #pragma unroll
   for (int q = 0; q < SG_MAXPP; ++q) acc[q] = 0.0;
   // pair index -> (i, j) with i <= j, row-major over the upper triangle
   for (int64_t p0 = (int64_t)blockIdx.x * TP; p0 < P; p0 += (int64_t)gridDim.x * TP) {
     __syncthreads();
+    const int64_t l0 = p0 % L, rr0 = p0 / L;  // once per tile; elements step l, wrapping rarely
     for (int e = tid; e < TP * K; e += SG_THREADS) {
       const int k = e / TP, pp = e % TP;
-      const int64_t pos = p0 + pp;
       double v = 0.0;
-      if (pos < P) {
-        const int64_t l = pos % L, rr = pos / L;
+      if (p0 + pp < P) {
+        int64_t l = l0 + pp, rr = rr0;
+        if (l >= L) { const int64_t w = l / L; l -= w * L; rr += w; }
         v = ld(x, l + L * (k + (int64_t)K * rr));
       }
-      sX[k * TP + pp] = v;
+      sX[k * TPS + pp] = v;
     }
     __syncthreads();
     if (npairs >= SG_THREADS) {
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(SG_THREADS) k_small_gram(const T* __restrict__
           while (rem >= K - i) { rem -= K - i; ++i; }
           const int j = i + rem;
           double s = 0.0;
-          for (int pp = 0; pp < TP; ++pp) s = fma(sX[i * TP + pp], sX[j * TP + pp], s);
+          for (int pp = 0; pp < TP; ++pp) s = fma(sX[i * TPS + pp], sX[j * TPS + pp], s);
           acc[q] += s;
         }
       }
@@ -125,7 +127,7 @@ __global__ void __launch_bounds__(SG_THREADS) k_small_gram(const T* __restrict__
       while (rem >= K - i) { rem -= K - i; ++i; }
       const int j = i + rem;
       double s = 0.0;
-      for (int pp = grp; pp < TP; pp += G) s = fma(sX[i * TP + pp], sX[j * TP + pp], s);
+      for (int pp = grp; pp < TP; pp += G) s = fma(sX[i * TPS + pp], sX[j * TPS + pp], s);
       acc[0] += s;
     }
   }
@@ -147,11 +149,17 @@ __global__ void __launch_bounds__(SG_THREADS) k_small_gram(const T* __restrict__
   }
 }
 
+// One warp per Gram pair: lanes take the block partials b = lane, lane+32, ...
+// (independent loads), then a fixed shuffle tree -- deterministic.
 __global__ void k_small_gram_reduce(const double* __restrict__ part, int nblk, int K, double* __restrict__ g) {
   const int npairs = K * (K + 1) / 2;
-  for (int pr = blockIdx.x * blockDim.x + threadIdx.x; pr < npairs; pr += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += part[(int64_t)b * npairs + pr];
+  const int lane = threadIdx.x & 31;
+  const int pr = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (pr >= npairs) return;
+  double s = 0.0;
+  for (int b = lane; b < nblk; b += 32) s += part[(int64_t)b * npairs + pr];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
     int i = 0, rem = pr;
     while (rem >= K - i) { rem -= K - i; ++i; }
     const int j = i + rem;
@@ -342,13 +350,13 @@ void small_gram(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t R
   const int64_t P = L * Rr;
   const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(P, TP), 2LL * c.num_sms));
   double* part = alloc<double>(c, (size_t)nblk * npairs);
-  const size_t smem = sizeof(double) * TP * K;
+  const size_t smem = sizeof(double) * (TP + 1) * K;
   if (tx == F32)
     k_small_gram<float><<<nblk, SG_THREADS, smem, c.stream>>>((const float*)x, L, (int)K, Rr, TP, part);
   else
     k_small_gram<double><<<nblk, SG_THREADS, smem, c.stream>>>((const double*)x, L, (int)K, Rr, TP, part);
   LAUNCHED("k_small_gram");
-  k_small_gram_reduce<<<(npairs + 255) / 256, 256, 0, c.stream>>>(part, nblk, (int)K, g);
+  k_small_gram_reduce<<<(unsigned)ceil_div((int64_t)npairs * 32, 256), 256, 0, c.stream>>>(part, nblk, (int)K, g);
   LAUNCHED("k_small_gram_reduce");
 }
 

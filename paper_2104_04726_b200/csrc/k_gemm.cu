@@ -27,7 +27,10 @@ namespace {
 #define TMB_GEMM_BM 64
 #endif
 // CTA tile BM x 64 x 16; warps of 32x32 (BM/32 along M, 2 along N)
-constexpr int BM = TMB_GEMM_BM, BN = 64, BK = 16, ST = TMB_GEMM_ST, WMW = BM / 32, NT = 32 * WMW * (BN / 32);
+#ifndef TMB_GEMM_BN
+#define TMB_GEMM_BN 64
+#endif
+constexpr int BM = TMB_GEMM_BM, BN = TMB_GEMM_BN, BK = 16, ST = TMB_GEMM_ST, WMW = BM / 32, NT = 32 * WMW * (BN / 32);
 constexpr int MINB = 512 / NT;  // resident CTAs per SM the register budget is sized for
 
 template <typename T> struct Pad;

@@ -638,17 +638,25 @@ __global__ void k_twisted(const double* __restrict__ d, const double* __restrict
 // T(0:i, i) = -tau_i T(0:i, 0:i) S(0:i, i) with S = V^T V.
 __global__ void k_larft(const double* __restrict__ S, const double* __restrict__ tau, int nb,
                         double* __restrict__ T) {
-  extern __shared__ double sT[];  // nb x nb column-major
+  extern __shared__ double sT[];  // nb x nb column-major T, then nb x nb S_p
+  double* sS = sT + nb * nb;
   const int p = blockIdx.x, r = threadIdx.x;
   const double* Sp = S + (int64_t)p * nb * nb;
   const double* tp = tau + (int64_t)p * nb;
+  for (int e = r; e < nb * nb; e += blockDim.x) sS[e] = Sp[e];  // S_p staged once (was re-read from L2 per step)
+  __syncthreads();
   for (int i = 0; i < nb; ++i) {
     if (r < nb) {
       double v = 0.0;
       if (r < i) {
-        double s = 0.0;
-        for (int c = r; c < i; ++c) s = fma(sT[r + nb * c], Sp[c + nb * i], s);
-        v = -tp[i] * s;
+        double s0 = 0.0, s1 = 0.0;  // two interleaved chains
+        int c = r;
+        for (; c + 1 < i; c += 2) {
+          s0 = fma(sT[r + nb * c], sS[c + nb * i], s0);
+          s1 = fma(sT[r + nb * (c + 1)], sS[c + 1 + nb * i], s1);
+        }
+        if (c < i) s0 = fma(sT[r + nb * c], sS[c + nb * i], s0);
+        v = -tp[i] * (s0 + s1);
       } else if (r == i) {
         v = tp[i];
       }
@@ -709,13 +717,14 @@ static void orthonormalize(Ctx& c, double* x, int64_t n, int64_t k) {
   c.arena.release(mk);
 }
 
-// Reflectors per compact-WY panel. 64 and 128 measured within 1% of each other
-// (scripts/ab_wy.sh); TMB_WY_NB selects 32/64/128 for A/B runs.
+// Reflectors per compact-WY panel: 64 (the fused k_apply_wy tile); TMB_WY_NB=32
+// selects the per-panel GEMM path for A/B runs (64 and 128 had measured within
+// 1 % on that path, scripts/ab_wy.sh; k_larft stages S_p, so nb <= 64).
 static int wy_nb() {
   static const int v = [] {
     const char* s = std::getenv("TMB_WY_NB");
     const int x = s ? std::atoi(s) : 64;
-    return (x == 32 || x == 64 || x == 128) ? x : 64;
+    return x == 32 ? 32 : 64;
   }();
   return v;
 }
@@ -904,10 +913,11 @@ static void backtransform(Ctx& c, const double* hv, const double* tau, int64_t n
   }
   static bool larft_attr = false;
   if (!larft_attr) {
-    TMB_CUDA(cudaFuncSetAttribute(k_larft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * 128 * 128)));
+    TMB_CUDA(cudaFuncSetAttribute(k_larft, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double) * 2 * 64 * 64)));
     larft_attr = true;
   }
-  k_larft<<<np, nb, sizeof(double) * nb * nb, c.stream>>>(S, tau, nb, T);
+  k_larft<<<np, nb, sizeof(double) * 2 * nb * nb, c.stream>>>(S, tau, nb, T);
   LAUNCHED("k_larft");
   // (A fused one-kernel variant that streams every panel through shared memory
   // measured 3.0 ms vs ~1 ms for these GEMMs at n=1920: it is smem-bandwidth

@@ -87,6 +87,17 @@ int tmb_color_f64(tmb_ctx* ctx, const double* px_dev, int64_t npx, int space, do
 int tmb_color_inv_f64(tmb_ctx* ctx, const double* px_dev, int64_t npx, int space,
                       double* out_dev, int64_t* n_clamped_host);
 
+/* Decode side: tensor_dev is a reconstructed coding-space
+ * stack (float64 F-order h x w x 3 x n_img: reconstruct(dequantize(q)),
+ * codec.py:446-447); every pixel goes through to_rgb (color.py:197-205).
+ * rgb_out_dev (nullable) receives interleaved float64 RGB images (n_img, h, w,
+ * 3). With rgb_dev (nullable; the original u8 images, same layout as
+ * tmb_color_u8's input) sse_host[n_img] receives each image's sum of squared
+ * differences in 8-bit units, sum((u8/255*255 - 255*rgb)^2): metrics.mse
+ * (metrics.py:16-23) times 3*h*w, as scene_psnr evaluates it (:41-76). */
+int tmb_decode_sse(tmb_ctx* ctx, const double* tensor_dev, int64_t n_img, int64_t h, int64_t w, int space,
+                   const uint8_t* rgb_dev, double* rgb_out_dev, double* sse_host);
+
 /* ---- tensor kernels (tensor.py) ---------------------------------------- */
 /* ttm (tensor.py:111-123): y = x x_mode m, m column-major rows x dims[mode]. */
 int tmb_ttm(tmb_ctx* ctx, const void* x_dev, int dtype, int order, const int64_t* dims, int mode,

@@ -19,7 +19,8 @@ __all__ = [
     "fro_norm", "hosvd", "t_hosvd", "hooi_sweep", "reconstruct", "fit",
     "pp_operators", "pp_sweep", "tucker_als", "Trace", "quantize_core",
     "dequantize_core", "preset_ranks", "rgb_to_ycbcr", "rgb_to_ipt",
-    "ycbcr_to_rgb", "ipt_to_rgb", "coding_tensor", "ORTHO_TOL", "PP_DIP_TOL",
+    "ycbcr_to_rgb", "ipt_to_rgb", "coding_tensor", "dequantize_model", "decode_stack", "scene_mse",
+    "ORTHO_TOL", "PP_DIP_TOL",
 ]
 
 ORTHO_TOL = 1e-8          # tucker.py:44
@@ -372,3 +373,36 @@ def coding_tensor(images_u8: np.ndarray, space: str) -> np.ndarray:
         for e in range(e_):
             out[:, :, :, v * e_ + e] = fn(images_u8[v, e].astype(np.float64) / 255.0)
     return out
+
+
+# ---------------------------------------------------------------- decode side
+def dequantize_model(levels: np.ndarray, step: float, factors):
+    """codec.py:137-148: core = levels * step, float32 factors upcast."""
+    return levels.astype(np.float64) * step, [np.asarray(f, dtype=np.float32).astype(np.float64) for f in factors]
+
+
+def decode_stack(core: np.ndarray, factors, space: str, views: int, exposures: int):
+    """reconstruct (tucker.py:166-171) then to_rgb per image (color.py:197-205):
+    (V, E, H, W, 3) float64 RGB from a (H, W, 3, V*E) model (tensor_to_stack's
+    plane order)."""
+    t = reconstruct(core, factors)
+    h, w, _, _ = t.shape
+    out = np.empty((views, exposures, h, w, 3))
+    for v in range(views):
+        for e in range(exposures):
+            px = np.ascontiguousarray(t[:, :, :, v * exposures + e])
+            if space == "ycbcr":
+                out[v, e] = ycbcr_to_rgb(px)
+            elif space == "ipt":
+                out[v, e] = ipt_to_rgb(px)
+            else:
+                out[v, e] = px
+    return out
+
+
+def scene_mse(images_u8: np.ndarray, rgb: np.ndarray) -> np.ndarray:
+    """metrics.mse(ref.pixels*255, test.pixels*255) per (view, exposure)
+    (metrics.py:16-23, as scene_psnr calls it at :58-62)."""
+    ref = images_u8.astype(np.float64) / 255.0 * 255.0
+    d = ref - rgb * 255.0
+    return np.mean(d * d, axis=(2, 3, 4))

@@ -135,6 +135,23 @@ int tmb_color_inv_f64(tmb_ctx* ctx, const double* px, int64_t npx, int space, do
   });
 }
 
+int tmb_decode_sse(tmb_ctx* ctx, const double* tensor, int64_t n_img, int64_t h, int64_t w, int space,
+                   const uint8_t* rgb, double* out_rgb, double* sse_host) {
+  return guard(ctx, [&](tmb::Ctx& c) {
+    if (space < TMB_SPACE_RGB || space > TMB_SPACE_IPT) throw Error(TMB_EINVAL, "unknown color space");
+    if (n_img < 0 || h < 0 || w < 0) throw Error(TMB_EINVAL, "negative stack shape");
+    if (rgb && !sse_host) throw Error(TMB_EINVAL, "sse_host is required with reference images");
+    const size_t mk = c.arena.mark();
+    double* sse = rgb ? tmb::alloc<double>(c, (size_t)std::max<int64_t>(n_img, 1)) : nullptr;
+    tmb::decode_sse(c, tensor, n_img, h, w, space, rgb, out_rgb, sse);
+    if (rgb && n_img > 0) {
+      TMB_CUDA(cudaMemcpyAsync(sse_host, sse, sizeof(double) * n_img, cudaMemcpyDeviceToHost, c.stream));
+      TMB_CUDA(cudaStreamSynchronize(c.stream));
+    }
+    c.arena.release(mk);
+  });
+}
+
 int tmb_ttm(tmb_ctx* ctx, const void* x, int dtype, int order, const int64_t* dims, int mode, const double* m,
             int64_t rows, double* y) {
   return guard(ctx, [&](tmb::Ctx& c) {

@@ -124,36 +124,109 @@ __global__ void k_color_f64(const double* __restrict__ px, int64_t npx, int spac
   }
 }
 
-// inverses (color.py:122-128, 161-182); clamp flags per pixel for ipt_to_rgb
+// inverses (color.py:122-128, 161-182) of one pixel; *cl = 1 if ipt_to_rgb clamped
+__device__ __forceinline__ void inv_px(int space, double a, double b, double c, double* o, int* cl) {
+  *cl = 0;
+  if (space == TMB_SPACE_YCBCR) {
+    const double r = add(a, mul(mul(2.0, 1.0 - KR), sub(c, 0.5)));
+    const double bb = add(a, mul(mul(2.0, 1.0 - KB), sub(b, 0.5)));
+    const double g = __ddiv_rn(sub(sub(a, mul(KR, r)), mul(KB, bb)), KG);
+    o[0] = r; o[1] = g; o[2] = bb;
+  } else if (space == TMB_SPACE_IPT) {
+    const double ipt[3] = {a, mul(2.0, sub(b, 0.5)), mul(2.0, sub(c, 0.5))};
+    double lmsp[3], lms[3], xyz[3], lin[3];
+    mat3(cc.ipt2lms, ipt, lmsp);
+    for (int k = 0; k < 3; ++k) lms[k] = spow(lmsp[k], 1.0 / 0.43);
+    mat3(cc.lms2xyz, lms, xyz);
+    mat3(cc.xyz2rgb, xyz, lin);
+    for (int k = 0; k < 3; ++k) {
+      const double v = fmin(fmax(lin[k], 0.0), 1.0);
+      if (v != lin[k]) *cl = 1;
+      o[k] = oetf(v);
+    }
+  } else {
+    o[0] = a; o[1] = b; o[2] = c;
+  }
+}
+
 __global__ void k_color_inv(const double* __restrict__ px, int64_t npx, int space, double* __restrict__ out,
                             int* __restrict__ clamped) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npx; i += (int64_t)gridDim.x * blockDim.x) {
-    const double a = px[3 * i], b = px[3 * i + 1], c = px[3 * i + 2];
     double o[3];
-    int cl = 0;
-    if (space == TMB_SPACE_YCBCR) {
-      const double r = add(a, mul(mul(2.0, 1.0 - KR), sub(c, 0.5)));
-      const double bb = add(a, mul(mul(2.0, 1.0 - KB), sub(b, 0.5)));
-      const double g = __ddiv_rn(sub(sub(a, mul(KR, r)), mul(KB, bb)), KG);
-      o[0] = r; o[1] = g; o[2] = bb;
-    } else if (space == TMB_SPACE_IPT) {
-      const double ipt[3] = {a, mul(2.0, sub(b, 0.5)), mul(2.0, sub(c, 0.5))};
-      double lmsp[3], lms[3], xyz[3], lin[3];
-      mat3(cc.ipt2lms, ipt, lmsp);
-      for (int k = 0; k < 3; ++k) lms[k] = spow(lmsp[k], 1.0 / 0.43);
-      mat3(cc.lms2xyz, lms, xyz);
-      mat3(cc.xyz2rgb, xyz, lin);
-      for (int k = 0; k < 3; ++k) {
-        const double v = fmin(fmax(lin[k], 0.0), 1.0);
-        if (v != lin[k]) cl = 1;
-        o[k] = oetf(v);
-      }
-    } else {
-      o[0] = a; o[1] = b; o[2] = c;
-    }
+    int cl;
+    inv_px(space, px[3 * i], px[3 * i + 1], px[3 * i + 2], o, &cl);
     out[3 * i] = o[0]; out[3 * i + 1] = o[1]; out[3 * i + 2] = o[2];
     clamped[i] = cl;
   }
+}
+
+// Decode side: the reconstructed coding-space stack
+// (F-order h x w x 3 x n_img fp64, reconstruct(dequantize(q)), codec.py:446-447)
+// -> to_rgb per pixel (color.py:197-205) -> optional interleaved RGB output and
+// the per-tile sum of squared 8-bit-unit errors against the original u8 images
+// (metrics.mse on pixels*255, metrics.py:16-23, as scene_psnr calls it, :41-76).
+// 32x32 pixel tiles: the fp64 planes are read along h (F-order, coalesced), the
+// u8 rows staged through shared memory along w.
+__global__ void __launch_bounds__(256) k_decode_sse(const double* __restrict__ t, int64_t h, int64_t w, int space,
+                                                    const uint8_t* __restrict__ rgb, double* __restrict__ out,
+                                                    double* __restrict__ part) {
+  __shared__ uint8_t su8[32][32 * 3 + 4];
+  __shared__ double red[8];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t img = blockIdx.z, h0 = (int64_t)blockIdx.y * 32, w0 = (int64_t)blockIdx.x * 32;
+  if (rgb) {
+    for (int r = ty; r < 32; r += 8) {
+      const int64_t hh = h0 + r;
+      if (hh >= h) continue;
+      const uint8_t* row = rgb + ((img * h + hh) * w + w0) * 3;
+      for (int bcol = tx; bcol < 96; bcol += 32)
+        if (w0 + bcol / 3 < w) su8[r][bcol] = row[bcol];
+    }
+    __syncthreads();
+  }
+  const int64_t hw = h * w;
+  const double* plane = t + 3 * hw * img;
+  double sse = 0.0;
+  for (int k = ty; k < 32; k += 8) {
+    const int64_t hh = h0 + tx, ww = w0 + k;
+    if (hh >= h || ww >= w) continue;
+    const int64_t p = hh + h * ww;
+    double o[3];
+    int cl;
+    inv_px(space, plane[p], plane[p + hw], plane[p + 2 * hw], o, &cl);
+    if (out) {
+      double* q = out + ((img * h + hh) * w + ww) * 3;
+      q[0] = o[0]; q[1] = o[1]; q[2] = o[2];
+    }
+    if (rgb) {
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        const double ref = mul(__ddiv_rn((double)su8[tx][k * 3 + ch], 255.0), 255.0);  // (u8/255)*255
+        const double d = sub(ref, mul(o[ch], 255.0));
+        sse = __fma_rn(d, d, sse);
+      }
+    }
+  }
+  if (!rgb) return;
+  for (int off = 16; off > 0; off >>= 1) sse += __shfl_xor_sync(0xffffffffu, sse, off);
+  if (tx == 0) red[ty] = sse;
+  __syncthreads();
+  if (tx == 0 && ty == 0) {
+    double s2 = 0.0;
+    for (int i = 0; i < 8; ++i) s2 += red[i];
+    part[img * (int64_t)gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = s2;
+  }
+}
+
+// per-image sum of its tile partials, fixed order (one warp per image)
+__global__ void k_sse_final(const double* __restrict__ part, int64_t tiles, int64_t n_img, double* __restrict__ sse) {
+  const int64_t img = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (img >= n_img) return;
+  double s = 0.0;
+  for (int64_t i = lane; i < tiles; i += 32) s += part[img * tiles + i];
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) sse[img] = s;
 }
 
 __global__ void k_count(const int* __restrict__ f, int64_t n, unsigned long long* __restrict__ cnt) {
@@ -244,6 +317,25 @@ void color_inv_f64(Ctx& c, const double* px, int64_t npx, int space, double* out
   TMB_CUDA(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, c.stream));
   TMB_CUDA(cudaStreamSynchronize(c.stream));
   if (n_clamped) *n_clamped = (int64_t)hc;
+  c.arena.release(mk);
+}
+
+void decode_sse(Ctx& c, const double* t, int64_t n_img, int64_t h, int64_t w, int space, const uint8_t* rgb,
+                double* out_rgb, double* sse_dev) {
+  if (n_img == 0 || h == 0 || w == 0) return;
+  ensure_constants(c);
+  const size_t mk = c.arena.mark();
+  dim3 grid((unsigned)ceil_div(w, 32), (unsigned)ceil_div(h, 32), (unsigned)n_img);
+  const int64_t tiles = (int64_t)grid.x * grid.y;
+  double* part = rgb ? alloc<double>(c, (size_t)(tiles * n_img)) : nullptr;
+  k_decode_sse<<<grid, dim3(32, 8), 0, c.stream>>>(t, h, w, space, rgb, out_rgb, part);
+  c.launches++;
+  check_launch("k_decode_sse");
+  if (rgb) {
+    k_sse_final<<<(unsigned)ceil_div(n_img, 8), 256, 0, c.stream>>>(part, tiles, n_img, sse_dev);
+    c.launches++;
+    check_launch("k_sse_final");
+  }
   c.arena.release(mk);
 }
 

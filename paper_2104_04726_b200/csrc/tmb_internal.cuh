@@ -146,5 +146,9 @@ void sytrd_tail(Ctx& c, double* A, int64_t n, int64_t K0, double* d, double* e, 
 void color_u8(Ctx& c, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, int space, float* out);
 void color_f64(Ctx& c, const double* rgb, int64_t npx, int space, double* out);
 void color_inv_f64(Ctx& c, const double* px, int64_t npx, int space, double* out, int64_t* n_clamped);
+// decode: coding-space F-order stack -> RGB (optional interleaved output) and the
+// per-image SSE in 8-bit units vs the original u8 images (rgb may be null)
+void decode_sse(Ctx& c, const double* t, int64_t n_img, int64_t h, int64_t w, int space, const uint8_t* rgb,
+                double* out_rgb, double* sse_dev);
 
 }  // namespace tmb

@@ -19,7 +19,8 @@ from . import _lib as L
 from .tensor import DenseTensor
 from .tucker import SolveConfig, SolveTrace, TuckerModel, _trace_buffers, _trace_from_c
 
-__all__ = ["StackResult", "encode_stack", "encode_stack_device", "coding_tensor"]
+__all__ = ["StackResult", "encode_stack", "encode_stack_device", "coding_tensor", "ScenePSNR", "DecodedStack",
+           "decode_stack"]
 
 
 @dataclass
@@ -99,3 +100,76 @@ def encode_stack(images_u8: np.ndarray, space: str, ranks: Sequence[int], sweeps
         facs = [L.host_f(f, (dims[n], ranks[n])) for n, f in enumerate(bufs["factors"])]
         model = TuckerModel(core, facs, dims)
     return StackResult(model, _trace_from_c(tr), levels, step, rel, bufs)
+
+
+# ---------------------------------------------------------------------------
+# decode side
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class ScenePSNR:
+    """metrics.ScenePSNR (metrics.py:33-38): per-view PSNR (8-bit units, MSE
+    averaged over exposures and channels) and the per-exposure (left, right) pairs."""
+
+    left: float
+    right: float
+    per_exposure: list[tuple[float, float]]
+
+
+@dataclass
+class DecodedStack:
+    rgb: np.ndarray | None       # (V, E, H, W, 3) float64 RGB, when requested
+    mse: np.ndarray | None       # (V, E) metrics.mse in 8-bit units vs the original images
+    psnr: ScenePSNR | None
+
+
+def _to_db(m: float) -> float:
+    import math
+
+    return math.inf if m == 0.0 else 10.0 * math.log10(255.0 * 255.0 / m)
+
+
+def decode_stack(q, space: str, views: int, exposures: int, images_u8=None, return_rgb: bool = True
+                 ) -> DecodedStack:
+    """Decode one stack on the device: ``dequantize`` (codec.py:137-148) ->
+    ``reconstruct`` (tucker.py:166-171) -> ``to_rgb`` per image (color.py:197-205),
+    and with ``images_u8`` (V, E, H, W, 3) the reference's ``scene_psnr``
+    (metrics.py:41-76) against them. ``q`` is a QuantizedModel of a (H, W, 3,
+    V*E) stack (or a TuckerModel, decoded without quantisation)."""
+    from .codec import QuantizedModel, dequantize
+
+    torch = L._torch()
+    model = dequantize(q) if isinstance(q, QuantizedModel) else q
+    h, w, c3, ve = model.source_dims
+    if c3 != 3 or ve != views * exposures:
+        raise ValueError(f"model dims {model.source_dims} are not a ({views}x{exposures})-image stack")
+    ranks = tuple(model.ranks)
+    hc = L.ctx()
+    core = L.dev_f64(model.core.array)
+    facs = [L.dev_f64(f) for f in model.factors]
+    rec = L.empty_f64(h * w * 3 * ve)
+    L.check(L.LIB.tmb_reconstruct(hc, 4, L.i64s(ranks), L.i64s(model.source_dims), L.ptr(core), L.ptrs(facs),
+                                  L.ptr(rec)), hc)
+    out = torch.empty(ve * h * w * 3, dtype=torch.float64, device="cuda") if return_rgb else None
+    src = None
+    sse = None
+    if images_u8 is not None:
+        if isinstance(images_u8, np.ndarray):
+            images_u8 = torch.from_numpy(np.ascontiguousarray(images_u8))
+        if tuple(images_u8.shape) != (views, exposures, h, w, 3) or images_u8.dtype != torch.uint8:
+            raise ValueError(f"reference images must be ({views}, {exposures}, {h}, {w}, 3) uint8")
+        src = images_u8.to("cuda").contiguous()
+        sse = np.zeros(ve, dtype=np.float64)
+    L.check(L.LIB.tmb_decode_sse(hc, L.ptr(rec), ve, h, w, L.SPACES[space], L.ptr(src) if src is not None else None,
+                                 L.ptr(out) if out is not None else None,
+                                 sse.ctypes.data_as(L.C.POINTER(L.C.c_double)) if sse is not None else None), hc)
+    rgb = out.cpu().numpy().reshape(views, exposures, h, w, 3) if out is not None else None
+    mse = psnr = None
+    if sse is not None:
+        mse = (sse / (3.0 * h * w)).reshape(views, exposures)
+        per_view = [_to_db(float(np.mean(mse[v]))) for v in range(views)]
+        per_exp = [[_to_db(float(m)) for m in mse[v]] for v in range(views)]
+        pairs = list(zip(per_exp[0], per_exp[1] if views > 1 else per_exp[0]))
+        psnr = ScenePSNR(per_view[0], per_view[1] if views > 1 else per_view[0], pairs)
+    return DecodedStack(rgb, mse, psnr)

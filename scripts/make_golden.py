@@ -28,10 +28,12 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, REF)
 sys.path.insert(0, str(ROOT))
 
-from tmcodec.codec import quantize_core  # noqa: E402
-from tmcodec.color import ColorImage, to_coding_space  # noqa: E402
+from tmcodec.codec import dequantize, quantize_core  # noqa: E402
+from tmcodec.metrics import mse as ref_mse, scene_psnr  # noqa: E402
+from tmcodec.sceneio import SceneStack  # noqa: E402
+from tmcodec.color import ColorImage, to_coding_space, to_rgb  # noqa: E402
 from tmcodec.tensor import DenseTensor  # noqa: E402
-from tmcodec.tucker import SolveConfig, reconstruct, tucker_als  # noqa: E402
+from tmcodec.tucker import SolveConfig, TuckerModel, reconstruct, tucker_als  # noqa: E402
 
 from paper_2104_04726_b200.synth import CONFIGS, make_stack, qp_for_bits  # noqa: E402
 
@@ -95,6 +97,36 @@ def run_case(name: str) -> None:
                      f"{platform.processor() or platform.machine()}; solve {dt:.2f}s"),
     )
     print(name, "fit", rows[-1][2], "rel", rel, f"{dt:.1f}s")
+
+
+def decode_case(name: str) -> None:
+    """Decode side through the reference: dequantize(quantize_core(model)) ->
+    reconstruct -> to_rgb per image -> scene_psnr / mse vs the original images,
+    for the model stored in tests/golden/<name>.npz."""
+    z = np.load(OUT / f"{name}.npz")
+    images = z["images"]
+    space = str(z["space"])
+    v_, e_, h, w, _ = images.shape
+    factors = [z[f"factor{n}"] for n in range(4)]
+    model = TuckerModel(DenseTensor(z["core"]), factors, (h, w, 3, v_ * e_))
+    q = quantize_core(model, int(z["qp"]))
+    t = reconstruct(dequantize(q)).array
+    mses = np.zeros((v_, e_))
+    ref_imgs, dec_imgs = {}, {}
+    for v in range(v_):
+        for e in range(e_):
+            ref_imgs[(v, e)] = ColorImage(images[v, e].astype(np.float64) / 255.0)
+            dec_imgs[(v, e)] = to_rgb(ColorImage(np.ascontiguousarray(t[:, :, :, v * e_ + e]), space))
+            mses[v, e] = ref_mse(ref_imgs[(v, e)].pixels * 255.0, dec_imgs[(v, e)].pixels * 255.0)
+    ref_scene = SceneStack(name, v_, e_, w, h, "rgb", ref_imgs)
+    dec_scene = SceneStack(name, v_, e_, w, h, "rgb", dec_imgs)
+    ps = scene_psnr(ref_scene, dec_scene)
+    rgb0 = dec_imgs[(0, 0)].pixels
+    sample = np.random.default_rng(7).integers(0, rgb0.size, 4096)
+    np.savez_compressed(OUT / f"decode_{name}.npz", mse=mses, psnr_left=np.array(ps.left),
+                        psnr_right=np.array(ps.right), per_exposure=np.array(ps.per_exposure),
+                        rgb00_sample_idx=sample, rgb00_sample=rgb0.ravel()[sample])
+    print("decode", name, ps.left, ps.right)
 
 
 def colour_kat() -> None:
@@ -169,10 +201,13 @@ def pp_cases() -> None:
 
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
-    names = sys.argv[1:] or (list(CASES) + ["colour", "api", "pp"])
+    names = sys.argv[1:] or (list(CASES) + ["colour", "api", "pp", "decode"])
     for nm in names:
         if nm == "colour":
             colour_kat()
+        elif nm == "decode":
+            for name in ("c1", "c2q"):
+                decode_case(name)
         elif nm == "api":
             api_cases()
         elif nm == "pp":

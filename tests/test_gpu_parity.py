@@ -108,3 +108,26 @@ def test_c1_full_config_exact_k():
         assert principal_angle(model.factors[n], z[f"factor{n}"]) < 1e-6
     q = tb.quantize_core(model, 51)
     assert int((q.levels != z["levels"]).sum()) == 0
+
+
+@pytest.mark.parametrize("name", ["c1", "c2q"])
+def test_decode_stack_matches_reference(golden, name):
+    """Device decode (dequantize -> reconstruct -> to_rgb -> scene_psnr) on the
+    reference's own model vs the reference's decode of it."""
+    z = np.load(__import__("conftest").GOLDEN / f"{name}.npz")
+    d = np.load(__import__("conftest").GOLDEN / f"decode_{name}.npz")
+    images = z["images"]
+    v_, e_, h, w, _ = images.shape
+    model = tb.TuckerModel(tb.DenseTensor(z["core"]), [z[f"factor{n}"] for n in range(4)], (h, w, 3, v_ * e_))
+    q = tb.quantize_core(model, int(z["qp"]))
+    assert int((q.levels != z["levels"]).sum()) == 0
+    out = tb.decode_stack(q, str(z["space"]), v_, e_, images_u8=images)
+    assert np.abs(out.rgb[0, 0].ravel()[d["rgb00_sample_idx"]] - d["rgb00_sample"]).max() < 1e-11
+    assert np.abs(out.mse - d["mse"]).max() / d["mse"].max() < 1e-11
+    assert abs(out.psnr.left - float(d["psnr_left"])) < 1e-8
+    assert abs(out.psnr.right - float(d["psnr_right"])) < 1e-8
+    for (a, b), (ra, rb) in zip(out.psnr.per_exposure, d["per_exposure"]):
+        assert abs(a - ra) < 1e-8 and abs(b - rb) < 1e-8
+    # decode without reference images: RGB only
+    out2 = tb.decode_stack(q, str(z["space"]), v_, e_)
+    assert out2.mse is None and np.array_equal(out2.rgb, out.rgb)

@@ -174,3 +174,23 @@ def test_oracle_fit_dual_formula():  # tests/test_tucker.py:193
     core, factors = oracle.t_hosvd(x, (3, 3, 2))
     assert abs(oracle.fit(x, core) - oracle.fit(x, core, factors, method="residual")) < 1e-10
     assert math.isfinite(oracle.fit(x, core))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2q"])
+def test_decode_matches_reference(name):
+    """Decode side (dequantize -> reconstruct -> to_rgb -> scene_psnr) vs the
+    reference run in this container (scripts/make_golden.py decode)."""
+    from conftest import GOLDEN
+
+    z = np.load(GOLDEN / f"{name}.npz")
+    d = np.load(GOLDEN / f"decode_{name}.npz")
+    images = z["images"]
+    v_, e_ = images.shape[:2]
+    levels, step = oracle.quantize_core(z["core"], int(z["qp"]))
+    core, facs = oracle.dequantize_model(levels, step, [z[f"factor{n}"] for n in range(4)])
+    rgb = oracle.decode_stack(core, facs, str(z["space"]), v_, e_)
+    assert np.abs(rgb[0, 0].ravel()[d["rgb00_sample_idx"]] - d["rgb00_sample"]).max() < 1e-12
+    mse = oracle.scene_mse(images, rgb)
+    assert np.abs(mse - d["mse"]).max() / d["mse"].max() < 1e-12
+    left = 10 * math.log10(255.0 ** 2 / float(np.mean(mse[0])))
+    assert abs(left - float(d["psnr_left"])) < 1e-9

@@ -515,6 +515,63 @@ __global__ void k_bisect(const double* __restrict__ d, const double* __restrict_
   if (lane == 0) vals[jd] = 0.5 * (lo + hi);
 }
 
+// W warps per eigenvalue (one block): 32W-way multisection, one shift per
+// lane, the warps' ballots combined through shared memory. Each round is one
+// Sturm chain long (latency-bound), so wider rounds (7 bits at W = 4 instead
+// of 5) mean fewer rounds; the 32W chains run on different warps in parallel.
+template <int W>
+__global__ void __launch_bounds__(32 * W) k_bisect_mw(const double* __restrict__ d, const double* __restrict__ e,
+                                                      int64_t n, int64_t k, double* __restrict__ vals) {
+  constexpr int NPT = 32 * W;
+  __shared__ unsigned masks[2][W];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t jd = blockIdx.x;
+  if (jd >= k) return;
+  const int64_t ja = n - 1 - jd;  // ascending index
+  double gl = 1e308, gu = -1e308, emax2 = 0.0;
+  for (int64_t i = lane; i < n; i += 32) {
+    const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
+    gl = fmin(gl, d[i] - r);
+    gu = fmax(gu, d[i] + r);
+    if (i + 1 < n) emax2 = fmax(emax2, e[i] * e[i]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+    gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+    emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
+  }
+  const double pivmin = DBL_MIN * fmax(1.0, emax2);
+  const double span = fmax(gu - gl, fmax(fabs(gl), fabs(gu)) * DBL_EPSILON);
+  double lo = gl - 2.0 * DBL_EPSILON * span - 2.0 * pivmin;
+  double hi = gu + 2.0 * DBL_EPSILON * span + 2.0 * pivmin;
+  for (int round = 0; round < 24; ++round) {
+    const double w = hi - lo;
+    if (w <= 2.0 * DBL_EPSILON * fmax(fabs(gl), fabs(gu)) + 4.0 * pivmin) break;
+    const int m = warp * 32 + lane;  // shift index, ascending in m
+    const auto shift = [&](int mm) { return lo + w * (double)(mm + 1) / (double)(NPT + 1); };
+    double x[1] = {shift(m)};
+    int c[1];
+    sturm_counts<1>(d, e, n, x, pivmin, c);
+    const unsigned above = __ballot_sync(0xffffffffu, c[0] > ja);
+    if (lane == 0) masks[round & 1][warp] = above;
+    __syncthreads();  // one barrier per round: the mask buffers alternate
+    int first = NPT;  // first shift whose count exceeds ja
+#pragma unroll
+    for (int q = W - 1; q >= 0; --q) {
+      const unsigned mq = masks[round & 1][q];
+      if (mq) first = q * 32 + __ffs(mq) - 1;
+    }
+    if (first == NPT) {
+      lo = shift(NPT - 1);  // eigenvalue above the last shift
+    } else {
+      const double xf = shift(first), xp = shift(first > 0 ? first - 1 : 0);
+      hi = xf;
+      if (first > 0) lo = xp;
+    }
+  }
+  if (threadIdx.x == 0) vals[jd] = 0.5 * (lo + hi);
+}
+
 // ------------------------------------------------------------------ twisted factorisation
 // One warp per eigenvalue: lane 0 runs the stationary (top-down) D+ chain while
 // lane 1 runs the progressive (bottom-up) D- chain; the twist index r =
@@ -1074,7 +1131,13 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
     Timed timed_tri(c, TAG_TRIDIAG, 0.0);
     // 2 warps (eigenvalues) per block: the counts are FP64-throughput bound, so
     // spread the k warps over all SMs (k/8 blocks of 8 warps left 60 % idle)
-    k_bisect<<<(unsigned)ceil_div(k, 2), 64, 0, c.stream>>>(d, e, n, k, vals);
+    static const int bis_w = [] {
+      const char* s = std::getenv("TMB_BISECT_WARPS");  // A/B: warps per eigenvalue (1, 2, 4)
+      return s ? std::atoi(s) : 2;  // measured: 1.15 / 1.25 / 1.37 ms tridiag at n=1920 for 2 / 1 / 4
+    }();
+    if (bis_w == 4) k_bisect_mw<4><<<(unsigned)k, 128, 0, c.stream>>>(d, e, n, k, vals);
+    else if (bis_w == 2) k_bisect_mw<2><<<(unsigned)k, 64, 0, c.stream>>>(d, e, n, k, vals);
+    else k_bisect<<<(unsigned)ceil_div(k, 2), 64, 0, c.stream>>>(d, e, n, k, vals);
     LAUNCHED("k_bisect");
     k_twisted<<<(unsigned)ceil_div(k, 2), 64, 0, c.stream>>>(d, e, n, k, vals, dp, dm, zs, vecs);
     LAUNCHED("k_twisted");

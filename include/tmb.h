@@ -81,6 +81,12 @@ int tmb_version(void);
  * (color.py:145-158) of u8/255 (sceneio.py:87), stacked as in SURVEY §8.0. */
 int tmb_color_u8(tmb_ctx* ctx, const uint8_t* rgb_dev, int64_t n_img, int64_t h, int64_t w,
                  int space, float* tensor_dev);
+/* The same colour transform into the reference codec's per-channel layout:
+ * three float32 F-order (h, w, E, V) tensors back to back (channel c at
+ * tensor_dev + c*h*w*n_img), i.e. stack_to_tensor(stack, c) for c = 0, 1, 2
+ * (sceneio.py:38, 191-199) of the converted stack (codec.py:389). */
+int tmb_color_u8_channels(tmb_ctx* ctx, const uint8_t* rgb_dev, int64_t n_img, int64_t h, int64_t w,
+                          int space, float* tensor_dev);
 /* Pixelwise float64 transforms on npx interleaved pixels (ColorImage.pixels):
  * to_coding_space (color.py:185-194) and to_rgb (color.py:197-205). */
 int tmb_color_f64(tmb_ctx* ctx, const double* px_dev, int64_t npx, int space, double* out_dev);
@@ -155,6 +161,16 @@ int tmb_quantize_core(tmb_ctx* ctx, const double* core_dev, int64_t n, int qp,
 /* dequantize core part (codec.py:137-148): core = levels * step. */
 int tmb_dequantize(tmb_ctx* ctx, const int64_t* levels_dev, int64_t n, double step,
                    double* core_dev);
+
+/* Latent-block level bytes: encode_ints / decode_ints (entropy.py:55-117) on
+ * the device -- zigzag map + LEB128 varints, low 7-bit group first. Encode
+ * writes at most cap bytes to out_dev and returns the byte count (EINVAL if
+ * cap is too small); decode reads count values and returns the bytes consumed
+ * (EINVAL "varint stream truncated ..." / "varint longer than 10 bytes"). */
+int tmb_varint_encode(tmb_ctx* ctx, const int64_t* levels_dev, int64_t n, uint8_t* out_dev, int64_t cap,
+                      int64_t* nbytes_host);
+int tmb_varint_decode(tmb_ctx* ctx, const uint8_t* in_dev, int64_t nbytes, int64_t count, int64_t* levels_dev,
+                      int64_t* used_host);
 
 /* ---- fused hot path ------------------------------------------------------
  * One stack end to end: u8 images -> colour (tmb_color_u8) -> tucker_als ->

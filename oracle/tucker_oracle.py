@@ -20,6 +20,7 @@ __all__ = [
     "pp_operators", "pp_sweep", "tucker_als", "Trace", "quantize_core",
     "dequantize_core", "preset_ranks", "rgb_to_ycbcr", "rgb_to_ipt",
     "ycbcr_to_rgb", "ipt_to_rgb", "coding_tensor", "dequantize_model", "decode_stack", "scene_mse",
+    "varint_encode_ints", "varint_decode_ints", "serialize_latent_channel",
     "ORTHO_TOL", "PP_DIP_TOL",
 ]
 
@@ -406,3 +407,53 @@ def scene_mse(images_u8: np.ndarray, rgb: np.ndarray) -> np.ndarray:
     ref = images_u8.astype(np.float64) / 255.0 * 255.0
     d = ref - rgb * 255.0
     return np.mean(d * d, axis=(2, 3, 4))
+
+
+# ---------------------------------------------------------------- latent block bytes
+def varint_encode_ints(values: np.ndarray) -> bytes:
+    """encode_ints (entropy.py:55-111): zigzag then LEB128, low group first."""
+    out = bytearray()
+    for v in np.asarray(values, dtype=np.int64).ravel():
+        u = ((int(v) << 1) ^ (int(v) >> 63)) & 0xFFFFFFFFFFFFFFFF
+        while True:
+            b = u & 0x7F
+            u >>= 7
+            if u:
+                out.append(b | 0x80)
+            else:
+                out.append(b)
+                break
+    return bytes(out)
+
+
+def varint_decode_ints(data: bytes, count: int):
+    """decode_ints (entropy.py:88-117): (int64 values, bytes consumed)."""
+    vals, pos = [], 0
+    for _ in range(count):
+        u, shift, nb = 0, 0, 0
+        while True:
+            if pos >= len(data):
+                raise ValueError("varint stream truncated")
+            b = data[pos]
+            pos += 1
+            nb += 1
+            u |= (b & 0x7F) << shift
+            shift += 7
+            if b < 0x80:
+                break
+        if nb > 10:
+            raise ValueError("varint longer than 10 bytes")
+        vals.append((u >> 1) ^ -(u & 1))
+    return np.array(vals, dtype=np.int64), pos
+
+
+def serialize_latent_channel(levels: np.ndarray, step: float, factors) -> bytes:
+    """_serialize_latent_channel (codec.py:285-291)."""
+    import struct
+
+    out = bytearray()
+    for f in factors:
+        out += np.asarray(f, dtype="<f4").tobytes(order="F")
+    out += varint_encode_ints(np.asarray(levels).ravel(order="F"))
+    out += struct.pack("<d", step)
+    return bytes(out)

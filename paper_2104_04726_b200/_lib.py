@@ -57,6 +57,9 @@ SIGNATURES = {
     "tmb_color_f64": ([_vp, _vp, _i64, _int, _vp], _int),
     "tmb_color_inv_f64": ([_vp, _vp, _i64, _int, _vp, _pi64], _int),
     "tmb_decode_sse": ([_vp, _vp, _i64, _i64, _i64, _int, _vp, _vp, C.POINTER(_dbl)], _int),
+    "tmb_color_u8_channels": ([_vp, _vp, _i64, _i64, _i64, _int, _vp], _int),
+    "tmb_varint_encode": ([_vp, _vp, _i64, _vp, _i64, _pi64], _int),
+    "tmb_varint_decode": ([_vp, _vp, _i64, _i64, _vp, _pi64], _int),
     "tmb_ttm": ([_vp, _vp, _int, _int, _pi64, _int, _vp, _i64, _vp], _int),
     "tmb_ttmc": ([_vp, _vp, _int, _int, _pi64, _pvp, _pi64, _pi64, _int, _int, _int, _vp], _int),
     "tmb_gram": ([_vp, _vp, _i64, _i64, _vp], _int),

@@ -1,14 +1,21 @@
 """Core quantiser of the latent path on the B200 (codec.py:78-148 of the reference).
 
 ``quantize_core`` / ``dequantize`` / ``QuantizedModel`` / ``preset_ranks`` /
-``CodecError``. The container, entropy stage and frames codec are outside the
-hot path and are not part of this package.
+``CodecError``, plus the latent path's callers and data format either side of
+the solve: ``solve_channels`` (the three per-channel
+solves of ``_solve_channels``, codec.py:366-374, on the device) and the latent
+block bytes (``_serialize_latent_channel`` / ``_deserialize_latent_channel``,
+codec.py:285-318, with the level varints encoded and decoded on the device).
+The container, range coder and frames codec are outside the hot path
+ and are not part of this package.
 """
 
 from __future__ import annotations
 
 import math
+import struct
 from dataclasses import dataclass
+from typing import Sequence
 
 import numpy as np
 
@@ -16,7 +23,8 @@ from . import _lib as L
 from .tensor import DenseTensor
 from .tucker import TuckerModel
 
-__all__ = ["CodecError", "QuantizedModel", "quantize_core", "dequantize", "preset_ranks", "PRESETS", "PRESET_RHO"]
+__all__ = ["CodecError", "QuantizedModel", "quantize_core", "dequantize", "preset_ranks", "PRESETS", "PRESET_RHO",
+           "serialize_latent_channel", "deserialize_latent_channel", "solve_channels"]
 
 PRESET_RHO = 0.25
 PRESETS = (1, 2, 3, 4, 5)
@@ -92,3 +100,94 @@ def dequantize(q: QuantizedModel) -> TuckerModel:
     model = TuckerModel(core, [np.asarray(f, dtype=np.float64) for f in q.factors], tuple(q.source_dims))
     model.validate(ortho_tol=1e-3)
     return model
+
+
+# ---------------------------------------------------------------------------
+# latent path: per-channel solves and the latent block bytes
+# ---------------------------------------------------------------------------
+
+
+def _varint_encode_dev(levels_dev, n: int) -> bytes:
+    torch = L._torch()
+    cap = max(1, 10 * n)
+    out = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    nb = L.C.c_int64()
+    h = L.ctx()
+    L.check(L.LIB.tmb_varint_encode(h, L.ptr(levels_dev), n, L.ptr(out), cap, L.C.byref(nb)), h)
+    return bytes(out[: nb.value].cpu().numpy().tobytes())
+
+
+def serialize_latent_channel(q: QuantizedModel) -> bytes:
+    """One channel's latent block (codec.py:285-291): float32 little-endian
+    column-major factors, the F-order levels as zigzag varints (encoded on the
+    device, entropy.py:55-111), then the float64 step."""
+    torch = L._torch()
+    out = bytearray()
+    for f in q.factors:
+        out += np.asarray(f, dtype="<f4").tobytes(order="F")
+    flat = np.ascontiguousarray(np.asarray(q.levels, dtype=np.int64).ravel(order="F"))
+    out += _varint_encode_dev(torch.from_numpy(flat).to("cuda"), flat.size)
+    out += struct.pack("<d", q.step)
+    return bytes(out)
+
+
+def deserialize_latent_channel(data: bytes, dims: Sequence[int], ranks: Sequence[int], qp: int) -> QuantizedModel:
+    """Inverse of serialize_latent_channel (codec.py:294-318), with the
+    reference's CodecError conditions; the varints are decoded on the device."""
+    torch = L._torch()
+    dims = tuple(int(d) for d in dims)
+    ranks = tuple(int(r) for r in ranks)
+    factor_bytes = sum(s * r * 4 for s, r in zip(dims, ranks))
+    if len(data) < factor_bytes + 8:
+        raise CodecError("latent block truncated")
+    factors, pos = [], 0
+    for s, r in zip(dims, ranks):
+        f = np.frombuffer(data, dtype="<f4", count=s * r, offset=pos)
+        factors.append(np.reshape(f, (s, r), order="F"))
+        pos += s * r * 4
+    (step,) = struct.unpack_from("<d", data, len(data) - 8)
+    count = int(np.prod(ranks))
+    body = np.frombuffer(data, dtype=np.uint8, count=len(data) - 8 - pos, offset=pos)
+    levels = torch.empty(max(count, 1), dtype=torch.int64, device="cuda")
+    src = torch.from_numpy(body.copy()).to("cuda") if body.size else torch.empty(1, dtype=torch.uint8, device="cuda")
+    used = L.C.c_int64()
+    h = L.ctx()
+    rc = L.LIB.tmb_varint_decode(h, L.ptr(src), int(body.size), count, L.ptr(levels), L.C.byref(used))
+    if rc != 0:
+        try:
+            L.check(rc, h)
+        except ValueError as exc:
+            raise CodecError(f"latent block corrupt: {exc}") from exc
+    if used.value != body.size:
+        raise CodecError(f"latent block has {body.size - used.value} trailing bytes")
+    lv = np.reshape(levels[:count].cpu().numpy(), ranks, order="F")
+    return QuantizedModel(dims, ranks, step, qp, lv, factors)
+
+
+def solve_channels(images_u8, space: str, ranks: Sequence[int], cfg, qp: int | None = None):
+    """The latent path's three per-channel solves on the device (codec.py:366-374
+    after the colour conversion of codec.py:389): the (V, E, H, W, 3) uint8 stack
+    is converted straight into three (H, W, E, V) float32 tensors
+    (stack_to_tensor, sceneio.py:191-199) and each is solved with ``cfg``
+    (a SolveConfig whose ranks are the (H, W, E, V) ranks). Returns a list of
+    (TuckerModel, SolveTrace), or of QuantizedModel when ``qp`` is given."""
+    from .tucker import solve_device
+
+    torch = L._torch()
+    if isinstance(images_u8, np.ndarray):
+        images_u8 = torch.from_numpy(np.ascontiguousarray(images_u8))
+    if images_u8.dtype != torch.uint8 or images_u8.dim() != 5 or images_u8.shape[-1] != 3:
+        raise ValueError("expected a (V, E, H, W, 3) uint8 image stack")
+    v, e, h, w, _ = images_u8.shape
+    dims = (h, w, e, v)
+    cfg.validate(dims)
+    src = images_u8.to("cuda").contiguous()
+    planes = torch.empty(3 * h * w * e * v, dtype=torch.float32, device="cuda")
+    hc = L.ctx()
+    L.check(L.LIB.tmb_color_u8_channels(hc, L.ptr(src), v * e, h, w, L.SPACES[space], L.ptr(planes)), hc)
+    per = h * w * e * v
+    out = []
+    for c in range(3):
+        model, trace = solve_device(planes[c * per:(c + 1) * per], L.F32, dims, cfg)
+        out.append(quantize_core(model, qp) if qp is not None else (model, trace))
+    return out

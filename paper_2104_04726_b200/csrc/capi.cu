@@ -121,6 +121,32 @@ int tmb_color_u8(tmb_ctx* ctx, const uint8_t* rgb, int64_t n_img, int64_t h, int
   });
 }
 
+int tmb_color_u8_channels(tmb_ctx* ctx, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, int space,
+                          float* out) {
+  return guard(ctx, [&](tmb::Ctx& c) {
+    if (space < TMB_SPACE_RGB || space > TMB_SPACE_IPT) throw Error(TMB_EINVAL, "unknown color space");
+    if (n_img < 0 || h < 0 || w < 0) throw Error(TMB_EINVAL, "negative image extent");
+    tmb::color_u8(c, rgb, n_img, h, w, space, out, true);
+  });
+}
+
+int tmb_varint_encode(tmb_ctx* ctx, const int64_t* levels, int64_t n, uint8_t* out, int64_t cap, int64_t* nbytes) {
+  return guard(ctx, [&](tmb::Ctx& c) {
+    if (n < 0 || cap < 0) throw Error(TMB_EINVAL, "negative size");
+    const int64_t b = tmb::varint_encode(c, levels, n, out, cap);
+    if (nbytes) *nbytes = b;
+  });
+}
+
+int tmb_varint_decode(tmb_ctx* ctx, const uint8_t* in, int64_t nbytes, int64_t count, int64_t* levels,
+                      int64_t* used) {
+  return guard(ctx, [&](tmb::Ctx& c) {
+    if (nbytes < 0 || count < 0) throw Error(TMB_EINVAL, "negative size");
+    const int64_t u = tmb::varint_decode(c, in, nbytes, count, levels);
+    if (used) *used = u;
+  });
+}
+
 int tmb_color_f64(tmb_ctx* ctx, const double* px, int64_t npx, int space, double* out) {
   return guard(ctx, [&](tmb::Ctx& c) {
     if (space < TMB_SPACE_RGB || space > TMB_SPACE_IPT) throw Error(TMB_EINVAL, "unknown color space");

@@ -74,8 +74,11 @@ __device__ __forceinline__ double oetf(double v) {
 }
 
 // 32x32 pixel tile per block, blockDim (32, 8)
+// channel_major = 0: planes (img, c) at (3 img + c) h w -- the BASELINE (H, W, 3, V*E) stack;
+// channel_major = 1: planes at (c n_img + img) h w -- three (H, W, E, V) tensors, one per
+// channel, the reference codec's stack_to_tensor layout (sceneio.py:38, 191-199).
 __global__ void __launch_bounds__(256) k_color_u8(const uint8_t* __restrict__ rgb, int64_t h, int64_t w,
-                                                  int space, float* __restrict__ out) {
+                                                  int space, float* __restrict__ out, int channel_major) {
   __shared__ float tile[3][32][33];  // [c][x][y]
   const int64_t img = blockIdx.z;
   const int64_t x0 = (int64_t)blockIdx.x * 32, y0 = (int64_t)blockIdx.y * 32;
@@ -100,11 +103,13 @@ __global__ void __launch_bounds__(256) k_color_u8(const uint8_t* __restrict__ rg
     }
   }
   __syncthreads();
-  float* dst = out + img * 3 * h * w;
+  const int64_t hw = h * w;
+  float* dst = out + img * (channel_major ? hw : 3 * hw);
+  const int64_t cstride = channel_major ? (int64_t)gridDim.z * hw : hw;
   for (int q = ty; q < 3 * 32; q += 8) {
     const int ch = q / 32, xx = q % 32;
     const int64_t x = x0 + xx, y = y0 + tx;
-    if (x < w && y < h) dst[y + h * (x + w * ch)] = tile[ch][xx][tx];
+    if (x < w && y < h) dst[y + h * x + cstride * ch] = tile[ch][xx][tx];
   }
 }
 
@@ -280,12 +285,13 @@ void ensure_constants(Ctx& c) {
 
 }  // namespace
 
-void color_u8(Ctx& c, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, int space, float* out) {
+void color_u8(Ctx& c, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, int space, float* out,
+              bool channel_major) {
   if (n_img == 0 || h == 0 || w == 0) return;
   ensure_constants(c);
   dim3 grid((unsigned)ceil_div(w, 32), (unsigned)ceil_div(h, 32), (unsigned)n_img);
   Timed timed(c, TAG_COLOR, 15.0 * (double)n_img * h * w);  // 3 B read + 12 B written per pixel
-  k_color_u8<<<grid, dim3(32, 8), 0, c.stream>>>(rgb, h, w, space, out);
+  k_color_u8<<<grid, dim3(32, 8), 0, c.stream>>>(rgb, h, w, space, out, channel_major ? 1 : 0);
   c.launches++;
   check_launch("k_color_u8");
 }

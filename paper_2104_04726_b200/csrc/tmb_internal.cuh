@@ -143,12 +143,19 @@ int64_t sytrd_tail_capacity(Ctx& c);
 void sytrd_tail(Ctx& c, double* A, int64_t n, int64_t K0, double* d, double* e, double* tau, double* hv);
 
 // ---------------------------------------------------------------- colour (k_color.cu)
-void color_u8(Ctx& c, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, int space, float* out);
+void color_u8(Ctx& c, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, int space, float* out,
+              bool channel_major = false);
 void color_f64(Ctx& c, const double* rgb, int64_t npx, int space, double* out);
 void color_inv_f64(Ctx& c, const double* px, int64_t npx, int space, double* out, int64_t* n_clamped);
 // decode: coding-space F-order stack -> RGB (optional interleaved output) and the
 // per-image SSE in 8-bit units vs the original u8 images (rgb may be null)
 void decode_sse(Ctx& c, const double* t, int64_t n_img, int64_t h, int64_t w, int space, const uint8_t* rgb,
                 double* out_rgb, double* sse_dev);
+
+// ---------------------------------------------------------------- latent block bytes (k_latent.cu)
+// zigzag + LEB128 varints of int64 levels (entropy.py:55-111); returns the byte count
+int64_t varint_encode(Ctx& c, const int64_t* levels, int64_t n, uint8_t* out, int64_t cap);
+// inverse (entropy.py:88-117); returns the bytes consumed, throws TMB_EINVAL when corrupt
+int64_t varint_decode(Ctx& c, const uint8_t* in, int64_t nbytes, int64_t count, int64_t* levels);
 
 }  // namespace tmb

@@ -28,7 +28,8 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, REF)
 sys.path.insert(0, str(ROOT))
 
-from tmcodec.codec import dequantize, quantize_core  # noqa: E402
+from tmcodec.codec import _serialize_latent_channel, dequantize, quantize_core  # noqa: E402
+from tmcodec.entropy import encode_ints  # noqa: E402
 from tmcodec.metrics import mse as ref_mse, scene_psnr  # noqa: E402
 from tmcodec.sceneio import SceneStack  # noqa: E402
 from tmcodec.color import ColorImage, to_coding_space, to_rgb  # noqa: E402
@@ -129,6 +130,23 @@ def decode_case(name: str) -> None:
     print("decode", name, ps.left, ps.right)
 
 
+def latent_case() -> None:
+    """Latent block bytes through the reference: quantize_core of the c1 golden
+    model, _serialize_latent_channel, and encode_ints on edge-case integers."""
+    z = np.load(OUT / "c1.npz")
+    v_, e_, h, w, _ = z["images"].shape
+    model = TuckerModel(DenseTensor(z["core"]), [z[f"factor{n}"] for n in range(4)], (h, w, 3, v_ * e_))
+    q = quantize_core(model, int(z["qp"]))
+    block = _serialize_latent_channel(q)
+    edge = np.array([0, 1, -1, 63, -64, 64, -65, 8191, -8192, 2**31, -(2**31), 2**62, -(2**62),
+                     2**63 - 1, -(2**63)], dtype=np.int64)
+    np.savez_compressed(OUT / "latent.npz", block=np.frombuffer(block, dtype=np.uint8), levels=q.levels,
+                        step=np.array(q.step), **{f"qfactor{n}": f for n, f in enumerate(q.factors)},
+                        dims=np.array((h, w, 3, v_ * e_)), ranks=np.array(q.ranks), qp=np.array(q.qp),
+                        edge=edge, edge_bytes=np.frombuffer(encode_ints(edge), dtype=np.uint8))
+    print("latent block", len(block), "bytes")
+
+
 def colour_kat() -> None:
     """Reference colour transforms on every gray level and 2000 random u8 triples."""
     rng = np.random.default_rng(5)
@@ -201,10 +219,12 @@ def pp_cases() -> None:
 
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
-    names = sys.argv[1:] or (list(CASES) + ["colour", "api", "pp", "decode"])
+    names = sys.argv[1:] or (list(CASES) + ["colour", "api", "pp", "decode", "latent"])
     for nm in names:
         if nm == "colour":
             colour_kat()
+        elif nm == "latent":
+            latent_case()
         elif nm == "decode":
             for name in ("c1", "c2q"):
                 decode_case(name)

@@ -131,3 +131,58 @@ def test_decode_stack_matches_reference(golden, name):
     # decode without reference images: RGB only
     out2 = tb.decode_stack(q, str(z["space"]), v_, e_)
     assert out2.mse is None and np.array_equal(out2.rgb, out.rgb)
+
+
+def test_latent_block_device_bytes_match_reference():
+    """Device zigzag-varint serialisation reproduces the reference's latent
+    block byte for byte, and deserialisation inverts it (codec.py:285-318)."""
+    z = np.load(__import__("conftest").GOLDEN / "latent.npz")
+    dims, ranks = tuple(int(d) for d in z["dims"]), tuple(int(r) for r in z["ranks"])
+    q = tb.QuantizedModel(dims, ranks, float(z["step"]), int(z["qp"]), z["levels"],
+                          [z[f"qfactor{n}"] for n in range(4)])
+    block = tb.serialize_latent_channel(q)
+    assert block == z["block"].tobytes()
+    back = tb.deserialize_latent_channel(block, dims, ranks, int(z["qp"]))
+    assert np.array_equal(back.levels, z["levels"]) and back.step == float(z["step"])
+    for a, b in zip(back.factors, q.factors):
+        assert np.array_equal(a, b)
+    # edge-case integers (int64 extremes) and corrupt / truncated blocks
+    edge = z["edge"]
+    qe = tb.QuantizedModel((1, 1, 1, edge.size), (1, 1, 1, edge.size), 1.0, 51, edge.reshape(1, 1, 1, -1),
+                           [np.ones((1, 1), np.float32)] * 3 + [np.eye(edge.size, dtype=np.float32)])
+    be = tb.serialize_latent_channel(qe)
+    assert be[12 + 4 * edge.size ** 2:-8] == z["edge_bytes"].tobytes()
+    assert np.array_equal(tb.deserialize_latent_channel(be, qe.source_dims, qe.ranks, 51).levels.ravel(), edge)
+    with pytest.raises(tb.CodecError, match="truncated"):
+        tb.deserialize_latent_channel(block[:-9] + block[-8:], dims, ranks, int(z["qp"]))
+    bad = bytearray(block)
+    nf = sum(s * r * 4 for s, r in zip(dims, ranks))
+    bad[nf:nf + 11] = b"\xff" * 10 + b"\x01"  # an 11-byte varint
+    with pytest.raises(tb.CodecError):
+        tb.deserialize_latent_channel(bytes(bad), dims, ranks, int(z["qp"]))
+    with pytest.raises(tb.CodecError, match="trailing"):
+        tb.deserialize_latent_channel(block[:-8] + b"\x00" + block[-8:], dims, ranks, int(z["qp"]))
+
+
+def test_solve_channels_match_oracle_per_channel():
+    """The latent path's three per-channel (H, W, E, V) solves (codec.py:366-374)
+    on the device vs the oracle on the same stack_to_tensor tensors."""
+    import oracle
+
+    cfg0 = CONFIGS["c1"]
+    images = make_stack(cfg0, seed=5, height=96, width=128)
+    v_, e_, h, w, _ = images.shape
+    ranks = (12, 16, e_, v_)
+    sc = tb.SolveConfig(ranks=ranks, max_sweeps=3, fit_tol=1e-300, pp_enter_tol=0.0)
+    got = tb.solve_channels(images, cfg0.space, ranks, sc)
+    t = oracle.coding_tensor(images, cfg0.space).astype(np.float32).astype(np.float64)  # (H, W, 3, V*E)
+    for c in range(3):
+        x = np.stack([t[:, :, c, vv * e_ + ee] for vv in range(v_) for ee in range(e_)], axis=2)
+        x = x.reshape(h, w, v_, e_).transpose(0, 1, 3, 2)  # (H, W, E, V)
+        core, facs, tr = oracle.tucker_als(np.asfortranarray(x), ranks, max_sweeps=3, fit_tol=1e-300, pp_enter_tol=0.0)
+        model, trace = got[c]
+        for n in range(4):
+            assert principal_angle(model.factors[n], facs[n]) < 1e-6
+        assert abs(trace.records[-1].fit - tr.rows[-1][2]) < 1e-10
+    q = tb.solve_channels(images, cfg0.space, ranks, sc, qp=51)
+    assert all(isinstance(x, tb.QuantizedModel) for x in q)

@@ -194,3 +194,16 @@ def test_decode_matches_reference(name):
     assert np.abs(mse - d["mse"]).max() / d["mse"].max() < 1e-12
     left = 10 * math.log10(255.0 ** 2 / float(np.mean(mse[0])))
     assert abs(left - float(d["psnr_left"])) < 1e-9
+
+
+def test_latent_block_bytes_match_reference():
+    """Latent block serialisation (codec.py:285-291, entropy.py:55-111) vs the
+    reference's own bytes (scripts/make_golden.py latent)."""
+    from conftest import GOLDEN
+
+    z = np.load(GOLDEN / "latent.npz")
+    block = oracle.serialize_latent_channel(z["levels"], float(z["step"]), [z[f"qfactor{n}"] for n in range(4)])
+    assert block == z["block"].tobytes()
+    assert oracle.varint_encode_ints(z["edge"]) == z["edge_bytes"].tobytes()
+    vals, used = oracle.varint_decode_ints(z["edge_bytes"].tobytes(), z["edge"].size)
+    assert np.array_equal(vals, z["edge"]) and used == z["edge_bytes"].size

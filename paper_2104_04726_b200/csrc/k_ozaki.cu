@@ -1,0 +1,399 @@
+// Ozaki-split fp64-equivalent TTM on the 5th-gen tensor cores (tcgen05.mma kind::i8).
+//
+// y = x x_n M  (ttm, tensor.py:111-123) for the full passes over the tensor.
+// GEMM view: rows m = (i, l) of x (i < L = prod(dims before n), l < R = prod
+// dims after n), K = dims[n], N = rows of M:  C(m, r) = sum_k A(m, k) B(k, r)
+// with A(m, k) = x[i + L k + L K l], B(k, r) = M(r, k).
+//
+// Split (Ozaki scheme, int8 digits): each row of A and each column of B is
+// scaled by a power of two 2^e so its entries lie in (-1, 1), then written as
+// 8 signed digits a = d0 2^-6 + sum_{s>=1} d_s 2^(-6-7s), |d| <= 64 (55 bits,
+// >= the 53 of an fp64 mantissa). A(m,k) B(k,r) then is a sum of digit
+// products d_s f_t 2^(-12-7(s+t)); the 36 products with s + t < 8 are kept
+// (the first dropped group is 2^-56 below the leading one, the fp64 GEMM's own
+// rounding level), each shift group g = s + t accumulating exactly in int32
+// (|d f| <= 2^12, <= 8 pairs per group, K <= 2^16).
+//
+// Kernel: one CTA per 128 (factor rows) x 64 (tensor rows) output tile,
+// warp-specialised. Lane 0 of warp 0 streams 64-byte K chunks of all 8 factor
+// digit planes (128 rows) and all 8 tensor digit planes (64 rows) with one 3-D TMA each (SWIZZLE_64B, the canonical
+// K-major SW64 UMMA layout) into a 2-stage ring; lane 0 of warp 1 issues the 72
+// tcgen05.mma (M=128, N=64, K=32) per chunk into 8 TMEM accumulators (8 x 64
+// of the 512 columns), one per shift group, committing each stage back to the
+// producer; then all 4 warps read the accumulators (tcgen05.ld 32x32b), form
+// sum_g acc_g 2^(-12-7g) in fp64, apply 2^(e_r + e_m) and store y. The grid
+// runs the tensor rows fastest, so the factor tile stays in L2 and the large
+// tensor digit planes are streamed ceil(N / 128) times.
+#include <cuda.h>
+
+#include <cstdlib>
+
+#include "tmb_internal.cuh"
+
+namespace tmb {
+namespace {
+
+constexpr int OZ_S = 8;                                   // digits per operand
+constexpr int OZ_BM = 128, OZ_BN = 64, OZ_BK = 64, OZ_ST = 2, OZ_NT = 128;
+constexpr uint32_t OZ_A_BYTES = OZ_S * OZ_BM * OZ_BK;    // 64 KB
+constexpr uint32_t OZ_B_BYTES = OZ_S * OZ_BN * OZ_BK;    // 32 KB
+constexpr uint32_t OZ_STAGE = OZ_A_BYTES + OZ_B_BYTES;  // 96 KB
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// 8 signed digits of v 2^-e in (-1, 1): the value scaled to a 55-bit fixed-point
+// integer (one rounding, at 2^-55 of the row/column maximum), then balanced
+// 7-bit digits by integer shifts: a = sum_s d_s 2^(-6-7s), |d_s| <= 64.
+__device__ __forceinline__ void digits8(double v, int e, int8_t (&d)[OZ_S]) {
+  long long A = __double2ll_rn(ldexp(v, 55 - e));
+#pragma unroll
+  for (int s = 0; s < OZ_S - 1; ++s) {
+    const int sh = 49 - 7 * s;
+    const long long q = (A + (1LL << (sh - 1))) >> sh;
+    d[s] = (int8_t)q;
+    A -= q << sh;
+  }
+  d[OZ_S - 1] = (int8_t)A;
+}
+
+__device__ __forceinline__ int exp_of(double mx) {  // smallest e with mx < 2^e (0 for mx == 0)
+  int e = 0;
+  if (mx > 0.0) frexp(mx, &e);
+  return e;
+}
+
+template <typename T>
+__device__ __forceinline__ double ldv(const T* p, int64_t i) { return (double)p[i]; }
+
+// row exponents of the x operand, rows m = (i, l): for L >= 32 a block covers 32
+// consecutive rows (lanes, coalesced along i) and its 8 warps split K; else a
+// warp per row with lanes along k
+template <typename T>
+__global__ void __launch_bounds__(256) k_oz_rowexp(const T* __restrict__ x, int64_t L, int64_t K, int64_t R,
+                                                   int* __restrict__ ea) {
+  const int64_t M = L * R;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (L >= 32) {
+    __shared__ double red[8][32];
+    const int64_t m = (int64_t)blockIdx.x * 32 + lane;
+    double mx = 0.0;
+    if (m < M) {
+      const int64_t i = m % L, l = m / L;
+      const T* p = x + i + L * K * l;
+      for (int64_t k = w; k < K; k += 8) mx = fmax(mx, fabs(ldv(p, L * k)));
+    }
+    red[w][lane] = mx;
+    __syncthreads();
+    if (w == 0 && m < M) {
+      for (int q = 1; q < 8; ++q) mx = fmax(mx, red[q][lane]);
+      ea[m] = exp_of(mx);
+    }
+  } else {
+    const int64_t m = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (m >= M) return;
+    const int64_t i = m % L, l = m / L;
+    const T* p = x + i + L * K * l;
+    double mx = 0.0;
+    for (int64_t k = lane; k < K; k += 32) mx = fmax(mx, fabs(ldv(p, L * k)));
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) ea[m] = exp_of(mx);
+  }
+}
+
+// x digits, K-major planes SA[s][m][k] (Mp x Kp, zero padded). Tiles of 32 rows
+// x 128 k through shared memory: reads coalesce along the contiguous index (i
+// when L >= 32, else k), writes are 4 packed digits (32 bits) per lane, 128 B per
+// plane row.
+template <typename T>
+__global__ void __launch_bounds__(256) k_oz_sliceA(const T* __restrict__ x, int64_t L, int64_t K, int64_t R,
+                                                   const int* __restrict__ ea, int64_t Mp, int64_t Kp,
+                                                   int8_t* __restrict__ sa) {
+  __shared__ __align__(16) int8_t tile[OZ_S][32][128 + 4];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // 8 warps
+  const int64_t M = L * R;
+  const int64_t m0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 128;
+  if (L >= 32) {  // lanes along m (i contiguous), warps over k
+    const int64_t m = m0 + lane;
+    const bool mok = m < M;
+    const int64_t i = mok ? m % L : 0, l = mok ? m / L : 0;
+    const int e = mok ? ea[m] : 0;
+    for (int kk = w; kk < 128; kk += 8) {
+      const int64_t k = k0 + kk;
+      int8_t d[OZ_S] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (mok && k < K) digits8(ldv(x, i + L * k + L * K * l), e, d);
+#pragma unroll
+      for (int s2 = 0; s2 < OZ_S; ++s2) tile[s2][lane][kk] = d[s2];
+    }
+  } else {  // lanes along k, warps over m
+    for (int mm = w; mm < 32; mm += 8) {
+      const int64_t m = m0 + mm;
+      const bool mok = m < M;
+      const int64_t i = mok ? m % L : 0, l = mok ? m / L : 0;
+      const int e = mok ? ea[m] : 0;
+      for (int kk = lane; kk < 128; kk += 32) {
+        const int64_t k = k0 + kk;
+        int8_t d[OZ_S] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (mok && k < K) digits8(ldv(x, i + L * k + L * K * l), e, d);
+#pragma unroll
+        for (int s2 = 0; s2 < OZ_S; ++s2) tile[s2][mm][kk] = d[s2];
+      }
+    }
+  }
+  __syncthreads();
+  for (int mm = w; mm < 32; mm += 8) {
+    const int64_t m = m0 + mm, k = k0 + 4 * lane;
+    if (m >= Mp || k >= Kp) continue;
+#pragma unroll
+    for (int s2 = 0; s2 < OZ_S; ++s2) {
+      const uint32_t v = (uint32_t)(uint8_t)tile[s2][mm][4 * lane] | ((uint32_t)(uint8_t)tile[s2][mm][4 * lane + 1] << 8) |
+                         ((uint32_t)(uint8_t)tile[s2][mm][4 * lane + 2] << 16) |
+                         ((uint32_t)(uint8_t)tile[s2][mm][4 * lane + 3] << 24);
+      *reinterpret_cast<uint32_t*>(sa + ((int64_t)s2 * Mp + m) * Kp + k) = v;
+    }
+  }
+}
+
+// B(k, n) = mat[n sMr + k sMk]: column exponents (warp per column) and digits SB[t][n][k]
+__global__ void k_oz_colexp(const double* __restrict__ mat, int64_t K, int64_t N, int64_t sMr, int64_t sMk,
+                            int* __restrict__ eb) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (n >= N) return;
+  double mx = 0.0;
+  for (int64_t k = lane; k < K; k += 32) mx = fmax(mx, fabs(mat[n * sMr + k * sMk]));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) eb[n] = exp_of(mx);
+}
+
+__global__ void k_oz_sliceB(const double* __restrict__ mat, int64_t K, int64_t N, int64_t sMr, int64_t sMk,
+                            const int* __restrict__ eb, int64_t Np, int64_t Kp, int8_t* __restrict__ sb) {
+  const int64_t total = Np * Kp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e % Kp, n = e / Kp;
+    int8_t d[OZ_S] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (n < N && k < K) digits8(mat[n * sMr + k * sMk], eb[n], d);
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) sb[((int64_t)s * Np + n) * Kp + k] = d[s];
+  }
+}
+
+__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;                 // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;        // SBO: 8 rows x 64 B
+  d |= (uint64_t)1 << 46;                 // descriptor version (sm100)
+  d |= (uint64_t)4 << 61;                 // SWIZZLE_64B
+  return d;
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  for (long long it = 0; it < 2000000000LL; ++it) {
+    uint32_t done;
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    if (done) return;
+  }
+  asm volatile("trap;");  // a protocol bug must not hang the GPU
+}
+
+// A operand (UMMA M side, 128 rows): factor digit planes, rows r (exponents eu);
+// B operand (UMMA N side, 64 rows): tensor digit planes, rows m = (i, l) (exponents ex).
+// The tensor digits -- the large operand -- are re-read once per 128 factor rows.
+__global__ void __launch_bounds__(OZ_NT, 1) k_oz_gemm(const __grid_constant__ CUtensorMap ta,
+                                                      const __grid_constant__ CUtensorMap tb,
+                                                      const int* __restrict__ eu, const int* __restrict__ ex,
+                                                      int64_t L, int64_t R, int64_t N, int64_t Kp,
+                                                      double* __restrict__ y) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[OZ_ST], empty[OZ_ST], done;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t m0 = (int64_t)blockIdx.y * OZ_BM, n0 = (int64_t)blockIdx.x * OZ_BN;
+  const int KT = (int)(Kp / OZ_BK);
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(saddr(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32) {
+    for (int s = 0; s < OZ_ST; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&empty[s])));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&done)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0 && lane == 0) {  // TMA producer: all 8 digit planes of A and of B per K chunk
+    for (int kt = 0; kt < KT; ++kt) {
+      const int st = kt % OZ_ST;
+      if (kt >= OZ_ST) mbar_wait(saddr(&empty[st]), ((kt / OZ_ST) - 1) & 1);
+      const uint32_t fb = saddr(&full[st]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(OZ_STAGE) : "memory");
+      const uint32_t da = saddr(sm + st * OZ_STAGE), db = da + OZ_A_BYTES;
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+          ::"r"(da), "l"(&ta), "r"(kt * OZ_BK), "r"((int)m0), "r"(0), "r"(fb) : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+          ::"r"(db), "l"(&tb), "r"(kt * OZ_BK), "r"((int)n0), "r"(0), "r"(fb) : "memory");
+    }
+  } else if (warp == 1 && lane == 0) {  // MMA issuer: 36 digit pairs x 2 K-halves per chunk
+    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) |
+                           ((uint32_t)(OZ_BM >> 4) << 24);
+    for (int kt = 0; kt < KT; ++kt) {
+      const int st = kt % OZ_ST;
+      mbar_wait(saddr(&full[st]), (kt / OZ_ST) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a0 = saddr(sm + st * OZ_STAGE), b0 = a0 + OZ_A_BYTES;
+#pragma unroll
+      for (int g = 0; g < OZ_S; ++g) {
+#pragma unroll
+        for (int s = 0; s <= g; ++s) {
+          const int t = g - s;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint64_t ad = sdesc_sw64(a0 + s * (OZ_BM * OZ_BK) + h * 32);
+            const uint64_t bd = sdesc_sw64(b0 + t * (OZ_BN * OZ_BK) + h * 32);
+            const uint32_t acc = (kt > 0 || s > 0 || h > 0) ? 1u : 0u;
+            asm volatile(
+                "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }"
+                ::"r"(tmem + (uint32_t)(g * OZ_BN)), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+          }
+        }
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                   ::"r"(saddr(&empty[st])));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(&done)));
+  }
+  __syncwarp();
+  mbar_wait(saddr(&done), 0);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  // epilogue: warp w holds factor rows r = m0 + 32w + lane (TMEM lanes); columns are
+  // tensor rows (i, l), 8 at a time -> 8 consecutive i of y for one r
+  const int64_t r = m0 + warp * 32 + lane;
+  const bool rok = r < N;
+  const int er = rok ? eu[r] : 0;
+  const int64_t MX = L * R;
+  for (int c0 = 0; c0 < OZ_BN; c0 += 8) {
+    uint32_t v[OZ_S][8];
+#pragma unroll
+    for (int g = 0; g < OZ_S; ++g)
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(v[g][0]), "=r"(v[g][1]), "=r"(v[g][2]), "=r"(v[g][3]), "=r"(v[g][4]), "=r"(v[g][5]),
+                     "=r"(v[g][6]), "=r"(v[g][7])
+                   : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(g * OZ_BN + c0)));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+    if (!rok) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t m = n0 + c0 + j;
+      if (m >= MX) continue;
+      double acc = 0.0;
+#pragma unroll
+      for (int g = OZ_S - 1; g >= 0; --g) acc += ldexp((double)(int32_t)v[g][j], -12 - 7 * g);  // small first
+      const int64_t i = m % L, l = m / L;
+      y[i + L * r + L * N * l] = ldexp(acc, er + ex[m]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    TMB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (!f || q != cudaDriverEntryPointSuccess) throw Error(TMB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    return (EncodeFn)f;
+  }();
+  return fn;
+}
+
+// 3-D map over digit planes [s][rows][Kp] (uint8), box (64 B of K, box_rows, 8 planes), SWIZZLE_64B
+CUtensorMap digit_map(int8_t* base, int64_t rows, int64_t Kp, uint32_t box_rows) {
+  CUtensorMap mp;
+  const cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)OZ_S};
+  const cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)(Kp * rows)};
+  const cuuint32_t box[3] = {(cuuint32_t)OZ_BK, box_rows, (cuuint32_t)OZ_S};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(&mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(TMB_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return mp;
+}
+
+}  // namespace
+
+bool ozaki_enabled() {
+  static const bool on = [] {
+    const char* s = std::getenv("TMB_OZAKI");  // 0 = DMMA for every contraction
+    return !(s && s[0] == '0');
+  }();
+  return on;
+}
+
+void ozaki_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t R, const double* mat, int64_t N,
+               int64_t sMr, int64_t sMk, double* y) {
+  const int64_t MX = L * R;  // tensor rows
+  const int64_t Xp = ceil_div(MX, OZ_BN) * OZ_BN, Up = ceil_div(N, OZ_BM) * OZ_BM, Kp = ceil_div(K, OZ_BK) * OZ_BK;
+  if (K > 65536) throw Error(TMB_EINVAL, "ozaki_ttm: K too large for int32 digit accumulation");
+  const size_t mk = c.arena.mark();
+  int* ex = alloc<int>(c, (size_t)Xp);
+  int* eu = alloc<int>(c, (size_t)Up);
+  int8_t* sx = alloc<int8_t>(c, (size_t)OZ_S * Xp * Kp);
+  int8_t* su = alloc<int8_t>(c, (size_t)OZ_S * Up * Kp);
+  // algorithmic work of the fp64-equivalent product: 2 MX N K
+  Timed timed(c, c.gemm_tag, 2.0 * (double)MX * N * K);
+  if (L >= 32) {
+    if (tx == F32) k_oz_rowexp<float><<<(unsigned)ceil_div(MX, 32), 256, 0, c.stream>>>((const float*)x, L, K, R, ex);
+    else k_oz_rowexp<double><<<(unsigned)ceil_div(MX, 32), 256, 0, c.stream>>>((const double*)x, L, K, R, ex);
+  } else {
+    if (tx == F32)
+      k_oz_rowexp<float><<<(unsigned)ceil_div(MX * 32, 256), 256, 0, c.stream>>>((const float*)x, L, K, R, ex);
+    else
+      k_oz_rowexp<double><<<(unsigned)ceil_div(MX * 32, 256), 256, 0, c.stream>>>((const double*)x, L, K, R, ex);
+  }
+  c.launches++;
+  check_launch("k_oz_rowexp");
+  dim3 ga((unsigned)ceil_div(Kp, 128), (unsigned)ceil_div(Xp, 32));
+  if (tx == F32) k_oz_sliceA<float><<<ga, 256, 0, c.stream>>>((const float*)x, L, K, R, ex, Xp, Kp, sx);
+  else k_oz_sliceA<double><<<ga, 256, 0, c.stream>>>((const double*)x, L, K, R, ex, Xp, Kp, sx);
+  c.launches++;
+  check_launch("k_oz_sliceA");
+  k_oz_colexp<<<(unsigned)ceil_div(N * 32, 256), 256, 0, c.stream>>>(mat, K, N, sMr, sMk, eu);
+  c.launches++;
+  check_launch("k_oz_colexp");
+  k_oz_sliceB<<<(unsigned)std::min<int64_t>(ceil_div(Up * Kp, 256), 16LL * c.num_sms), 256, 0, c.stream>>>(
+      mat, K, N, sMr, sMk, eu, Up, Kp, su);
+  c.launches++;
+  check_launch("k_oz_sliceB");
+  const CUtensorMap ta = digit_map(su, Up, Kp, OZ_BM), tb = digit_map(sx, Xp, Kp, OZ_BN);
+  const size_t smem = (size_t)OZ_ST * OZ_STAGE + 1024;
+  static bool attr = false;
+  if (!attr) {
+    TMB_CUDA(cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  dim3 grid((unsigned)(Xp / OZ_BN), (unsigned)(Up / OZ_BM));
+  k_oz_gemm<<<grid, OZ_NT, smem, c.stream>>>(ta, tb, eu, ex, L, R, N, Kp, y);
+  c.launches++;
+  check_launch("k_oz_gemm");
+  c.arena.release(mk);
+}
+
+}  // namespace tmb

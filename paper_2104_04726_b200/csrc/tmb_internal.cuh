@@ -152,6 +152,13 @@ void color_inv_f64(Ctx& c, const double* px, int64_t npx, int space, double* out
 void decode_sse(Ctx& c, const double* t, int64_t n_img, int64_t h, int64_t w, int space, const uint8_t* rgb,
                 double* out_rgb, double* sse_dev);
 
+// ---------------------------------------------------------------- Ozaki TTM on tcgen05 (k_ozaki.cu)
+// y = x x_n mat over the GEMM view rows (i < L, l < R), K = dims[n], N = rows of mat
+// (mat(r, k) at mat[r sMr + k sMk]); fp64-equivalent via int8 digit products.
+bool ozaki_enabled();
+void ozaki_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t R, const double* mat, int64_t N,
+               int64_t sMr, int64_t sMk, double* y);
+
 // ---------------------------------------------------------------- latent block bytes (k_latent.cu)
 // zigzag + LEB128 varints of int64 levels (entropy.py:55-111); returns the byte count
 int64_t varint_encode(Ctx& c, const int64_t* levels, int64_t n, uint8_t* out, int64_t cap);

@@ -186,3 +186,26 @@ def test_solve_channels_match_oracle_per_channel():
         assert abs(trace.records[-1].fit - tr.rows[-1][2]) < 1e-10
     q = tb.solve_channels(images, cfg0.space, ranks, sc, qp=51)
     assert all(isinstance(x, tb.QuantizedModel) for x in q)
+
+
+def test_ozaki_tcgen05_ttm_matches_fp64():
+    """The Ozaki int8-digit TTM on tcgen05 (k_ozaki.cu) for a >= 8 GFLOP mode-1
+    full pass: fp64-class agreement with a float64 reference contraction."""
+    import torch
+
+    from paper_2104_04726_b200 import _lib as L
+
+    dims = (512, 1024, 3, 8)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.rand(int(np.prod(dims)), dtype=torch.float32, device="cuda", generator=g) ** 3
+    u = torch.linalg.qr(torch.randn(1024, 512, dtype=torch.float64, device="cuda", generator=g))[0]
+    y = torch.empty(512 * 512 * 3 * 8, dtype=torch.float64, device="cuda")
+    h = L.ctx()
+    n0 = L.launch_count()
+    L.check(L.LIB.tmb_ttm(h, L.ptr(x), L.F32, 4, L.i64s(dims), 1, L.ptr(u.contiguous().view(-1)), 512, L.ptr(y)), h)
+    assert L.launch_count() - n0 >= 5  # digit split + tcgen05 GEMM, not the DMMA path
+    ref = torch.einsum("lcji,jr->lcri", x.double().view(8, 3, 1024, 512), u)
+    err = (y.view(8, 3, 512, 512) - ref)
+    scale = torch.einsum("lcji,jr->lcri", x.double().view(8, 3, 1024, 512).abs(), u.abs())
+    assert (err.abs() / scale).max().item() < 4e-15
+    assert (err.norm() / ref.norm()).item() < 4e-15

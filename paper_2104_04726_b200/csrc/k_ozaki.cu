@@ -41,11 +41,27 @@ constexpr uint32_t OZ_STAGE = OZ_A_BYTES + OZ_B_BYTES;  // 96 KB
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-// 8 signed digits of v 2^-e in (-1, 1): the value scaled to a 55-bit fixed-point
-// integer (one rounding, at 2^-55 of the row/column maximum), then balanced
-// 7-bit digits by integer shifts: a = sum_s d_s 2^(-6-7s), |d_s| <= 64.
-__device__ __forceinline__ void digits8(double v, int e, int8_t (&d)[OZ_S]) {
-  long long A = __double2ll_rn(ldexp(v, 55 - e));
+// v 2^(55-e) rounded to an integer (|v| < 2^e): one rounding at 2^-55 of the
+// row/column maximum. fp32 inputs take an integer-only path from the bit pattern.
+__device__ __forceinline__ long long fixed55(double v, int e) { return __double2ll_rn(ldexp(v, 55 - e)); }
+__device__ __forceinline__ long long fixed55(float v, int e) {
+  const uint32_t b = __float_as_uint(v);
+  const int ex = (int)((b >> 23) & 0xFF);
+  long long mant = (long long)(b & 0x7FFFFF);
+  int sh;
+  if (ex == 0) sh = 1 - 150 + 55 - e;  // subnormal
+  else { mant |= 0x800000; sh = ex - 150 + 55 - e; }
+  long long a;
+  if (sh >= 0) a = mant << sh;
+  else if (sh > -40) a = (mant + (1LL << (-sh - 1))) >> (-sh);  // round half up (ties are measure-zero)
+  else a = 0;
+  return (b >> 31) ? -a : a;
+}
+
+// balanced 7-bit digits of the fixed-point value: a = sum_s d_s 2^(-6-7s), |d_s| <= 64
+template <typename T>
+__device__ __forceinline__ void digits8(T v, int e, int8_t (&d)[OZ_S]) {
+  long long A = fixed55(v, e);
 #pragma unroll
   for (int s = 0; s < OZ_S - 1; ++s) {
     const int sh = 49 - 7 * s;
@@ -64,6 +80,8 @@ __device__ __forceinline__ int exp_of(double mx) {  // smallest e with mx < 2^e 
 
 template <typename T>
 __device__ __forceinline__ double ldv(const T* p, int64_t i) { return (double)p[i]; }
+template <typename T>
+__device__ __forceinline__ T ldraw(const T* p, int64_t i) { return p[i]; }
 
 // row exponents of the x operand, rows m = (i, l): for L >= 32 a block covers 32
 // consecutive rows (lanes, coalesced along i) and its 8 warps split K; else a
@@ -120,7 +138,7 @@ __global__ void __launch_bounds__(256) k_oz_sliceA(const T* __restrict__ x, int6
     for (int kk = w; kk < 128; kk += 8) {
       const int64_t k = k0 + kk;
       int8_t d[OZ_S] = {0, 0, 0, 0, 0, 0, 0, 0};
-      if (mok && k < K) digits8(ldv(x, i + L * k + L * K * l), e, d);
+      if (mok && k < K) digits8(ldraw(x, i + L * k + L * K * l), e, d);
 #pragma unroll
       for (int s2 = 0; s2 < OZ_S; ++s2) tile[s2][lane][kk] = d[s2];
     }
@@ -133,7 +151,7 @@ __global__ void __launch_bounds__(256) k_oz_sliceA(const T* __restrict__ x, int6
       for (int kk = lane; kk < 128; kk += 32) {
         const int64_t k = k0 + kk;
         int8_t d[OZ_S] = {0, 0, 0, 0, 0, 0, 0, 0};
-        if (mok && k < K) digits8(ldv(x, i + L * k + L * K * l), e, d);
+        if (mok && k < K) digits8(ldraw(x, i + L * k + L * K * l), e, d);
 #pragma unroll
         for (int s2 = 0; s2 < OZ_S; ++s2) tile[s2][mm][kk] = d[s2];
       }

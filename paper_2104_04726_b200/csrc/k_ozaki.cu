@@ -22,8 +22,8 @@
 // of the 512 columns), one per shift group, committing each stage back to the
 // producer; then all 4 warps read the accumulators (tcgen05.ld 32x32b), form
 // sum_g acc_g 2^(-12-7g) in fp64, apply 2^(e_r + e_m) and store y. The grid
-// runs the tensor rows fastest, so the factor tile stays in L2 and the large
-// tensor digit planes are streamed ceil(N / 128) times.
+// runs the factor-row tiles fastest, so the CTAs sharing a tensor tile read its
+// digit planes from HBM once (the factor digits stay in L2).
 #include <cuda.h>
 
 #include <cstdlib>
@@ -228,7 +228,9 @@ __global__ void __launch_bounds__(OZ_NT, 1) k_oz_gemm(const __grid_constant__ CU
   __shared__ __align__(8) uint64_t full[OZ_ST], empty[OZ_ST], done;
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t m0 = (int64_t)blockIdx.y * OZ_BM, n0 = (int64_t)blockIdx.x * OZ_BN;
+  // factor-row tiles fastest: the CTAs sharing one tensor tile run together, so
+  // its digit planes are read from HBM once and from L2 by the others
+  const int64_t m0 = (int64_t)blockIdx.x * OZ_BM, n0 = (int64_t)blockIdx.y * OZ_BN;
   const int KT = (int)(Kp / OZ_BK);
 
   if (warp == 0) {
@@ -270,6 +272,9 @@ __global__ void __launch_bounds__(OZ_NT, 1) k_oz_gemm(const __grid_constant__ CU
       mbar_wait(saddr(&full[st]), (kt / OZ_ST) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t a0 = saddr(sm + st * OZ_STAGE), b0 = a0 + OZ_A_BYTES;
+      // descriptors differ only in the 14-bit start-address field (16-byte units):
+      // build each stage's base once, add compile-time plane / K-half offsets
+      const uint64_t adb = sdesc_sw64(a0), bdb = sdesc_sw64(b0);
 #pragma unroll
       for (int g = 0; g < OZ_S; ++g) {
 #pragma unroll
@@ -277,8 +282,8 @@ __global__ void __launch_bounds__(OZ_NT, 1) k_oz_gemm(const __grid_constant__ CU
           const int t = g - s;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const uint64_t ad = sdesc_sw64(a0 + s * (OZ_BM * OZ_BK) + h * 32);
-            const uint64_t bd = sdesc_sw64(b0 + t * (OZ_BN * OZ_BK) + h * 32);
+            const uint64_t ad = adb + (uint64_t)((s * (OZ_BM * OZ_BK) + h * 32) >> 4);
+            const uint64_t bd = bdb + (uint64_t)((t * (OZ_BN * OZ_BK) + h * 32) >> 4);
             const uint32_t acc = (kt > 0 || s > 0 || h > 0) ? 1u : 0u;
             asm volatile(
                 "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }"
@@ -316,7 +321,8 @@ __global__ void __launch_bounds__(OZ_NT, 1) k_oz_gemm(const __grid_constant__ CU
       if (m >= MX) continue;
       double acc = 0.0;
 #pragma unroll
-      for (int g = OZ_S - 1; g >= 0; --g) acc += ldexp((double)(int32_t)v[g][j], -12 - 7 * g);  // small first
+      for (int g = OZ_S - 1; g >= 0; --g)  // small first; 2^(-12-7g) exact constants
+        acc = fma((double)(int32_t)v[g][j], __longlong_as_double((long long)(1023 - 12 - 7 * g) << 52), acc);
       const int64_t i = m % L, l = m / L;
       y[i + L * r + L * N * l] = ldexp(acc, er + ex[m]);
     }
@@ -407,7 +413,7 @@ void ozaki_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t R,
     TMB_CUDA(cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  dim3 grid((unsigned)(Xp / OZ_BN), (unsigned)(Up / OZ_BM));
+  dim3 grid((unsigned)(Up / OZ_BM), (unsigned)(Xp / OZ_BN));
   k_oz_gemm<<<grid, OZ_NT, smem, c.stream>>>(ta, tb, eu, ex, L, R, N, Kp, y);
   c.launches++;
   check_launch("k_oz_gemm");

@@ -229,7 +229,7 @@ def run_ours(args) -> None:
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     fam = {}
     for tag, name in ((0, "gemm_dmma"), (1, "sytrd"), (2, "tridiag_vectors"), (3, "color_u8"),
-                      (4, "eig_gemm_dmma")):
+                      (4, "eig_gemm_dmma"), (5, "ttm_ozaki_i8")):
         cnt, tms, work = L.C.c_int64(), L.C.c_double(), L.C.c_double()
         L.check(L.LIB.tmb_timing_read(h, tag, L.C.byref(cnt), L.C.byref(tms), L.C.byref(work)), h)
         fam[name] = {"launches": cnt.value, "ms": tms.value, "work": work.value}

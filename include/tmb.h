@@ -66,10 +66,11 @@ const char* tmb_last_error(const tmb_ctx* ctx);
 int64_t tmb_launch_count(const tmb_ctx* ctx); /* kernels launched so far */
 /* Launch timing by kernel family (CUDA events on the context stream), used by
  * bench.py for the roofline: tags 0 DMMA GEMM (TTM/Gram), 1 tridiagonalisation,
- * 2 bisection+twisted vectors, 3 colour, 4 DMMA GEMMs inside the eigen-solver. tmb_timing(ctx, 1)
+ * 2 bisection+twisted vectors, 3 colour, 4 DMMA GEMMs inside the eigen-solver, 5 Ozaki int8
+ * tcgen05 TTM (digit split + GEMM; work in fp64-equivalent flops). tmb_timing(ctx, 1)
  * resets and enables; tmb_timing_read returns launches, total ms and the
  * algorithmic work (flops, or bytes for colour) attributed to the tag. */
-enum { TMB_TAG_GEMM = 0, TMB_TAG_SYTRD = 1, TMB_TAG_TRIDIAG = 2, TMB_TAG_COLOR = 3, TMB_TAG_EIG_GEMM = 4 };
+enum { TMB_TAG_GEMM = 0, TMB_TAG_SYTRD = 1, TMB_TAG_TRIDIAG = 2, TMB_TAG_COLOR = 3, TMB_TAG_EIG_GEMM = 4, TMB_TAG_OZAKI = 5 };
 int tmb_timing(tmb_ctx* ctx, int enable);
 int tmb_timing_read(tmb_ctx* ctx, int tag, int64_t* count, double* ms, double* work);
 int tmb_version(void);

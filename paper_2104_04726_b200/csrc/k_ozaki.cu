@@ -382,7 +382,7 @@ void ozaki_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t R,
   int8_t* sx = alloc<int8_t>(c, (size_t)OZ_S * Xp * Kp);
   int8_t* su = alloc<int8_t>(c, (size_t)OZ_S * Up * Kp);
   // algorithmic work of the fp64-equivalent product: 2 MX N K
-  Timed timed(c, c.gemm_tag, 2.0 * (double)MX * N * K);
+  Timed timed(c, TAG_OZAKI, 2.0 * (double)MX * N * K);  // fp64-equivalent flops
   if (L >= 32) {
     if (tx == F32) k_oz_rowexp<float><<<(unsigned)ceil_div(MX, 32), 256, 0, c.stream>>>((const float*)x, L, K, R, ex);
     else k_oz_rowexp<double><<<(unsigned)ceil_div(MX, 32), 256, 0, c.stream>>>((const double*)x, L, K, R, ex);

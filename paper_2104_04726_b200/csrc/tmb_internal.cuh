@@ -58,7 +58,7 @@ struct KernelTimes {
   struct Rec { int tag; size_t a, b; double work; };
   std::vector<Rec> recs;
 };
-enum TimerTag { TAG_GEMM = 0, TAG_SYTRD, TAG_TRIDIAG, TAG_COLOR, TAG_EIG_GEMM, TAG_COUNT };
+enum TimerTag { TAG_GEMM = 0, TAG_SYTRD, TAG_TRIDIAG, TAG_COLOR, TAG_EIG_GEMM, TAG_OZAKI, TAG_COUNT };
 
 struct Ctx {
   int device = 0;

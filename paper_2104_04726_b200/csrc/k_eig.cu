@@ -1092,6 +1092,11 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
     const int64_t tail_m = std::min(cap, tail_env);
     K0 = tail_m >= 2 ? std::max<int64_t>(0, n - 1 - tail_m) : n;
   }
+  // Grid-wide kernels stop when the trailing block fits one CTA's shared
+  // memory; the single-CTA kernel finishes it with block barriers only.
+  const int64_t t1 = sytrd_tail1_max();
+  const bool tail1 = K0 == n && tail_env < 0 && t1 >= 2 && n - 1 > t1;
+  if (tail1) K0 = n - 1 - t1;
   static const bool prof_on = std::getenv("TMB_TRD_PROFILE") != nullptr;
   long long* prof = nullptr;
   if (prof_on) {
@@ -1107,7 +1112,8 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
       TMB_CUDA(cudaLaunchCooperativeKernel(kern, blocks, TRD_THREADS, args, smem, c.stream));
       LAUNCHED("k_sytrd");
     }
-    if (K0 < n) sytrd_tail(c, A, n, K0, d, e, tau, hv);
+    if (tail1) sytrd_tail1(c, A, n, K0, d, e, tau, hv);
+    else if (K0 < n) sytrd_tail(c, A, n, K0, d, e, tau, hv);
   }
   if (prof && K0 > 0) {  // diagnostics: mean cycles per phase over the sampled steps/blocks
     long long h[3 * 8 * 8];

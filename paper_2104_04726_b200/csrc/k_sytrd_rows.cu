@@ -61,7 +61,11 @@ __device__ __forceinline__ double bsum(double v, double* red, int& phase) {
   __syncthreads();
   double t[NW];
 #pragma unroll
-  for (int i = 0; i < NW; ++i) t[i] = r[i];
+  for (int i = 0; i < NW; i += 2) {  // 16-byte broadcast loads: half the LSU instructions
+    const double2 q = *reinterpret_cast<const double2*>(r + i);
+    t[i] = q.x;
+    t[i + 1] = q.y;
+  }
 #pragma unroll
   for (int h = NW / 2; h > 0; h >>= 1)
 #pragma unroll
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
   double* A = a.A;
   extern __shared__ double sm[];
   double* cols = sm;                          // qmax x N, column q = jb + NB q
-  double* part = cols + (size_t)qmax * N;     // NW x qmax per-warp partial dots
+  double* part = cols + ((size_t)qmax * N + 1) / 2 * 2;  // NW x qmax per-warp partial dots (16-B aligned)
   double* red = part + NW * qmax;             // 2 x NW
   double* vo = red + 2 * NW;                  // qmax: v_k at the owned column indices
   double* wo = vo + qmax;                     // qmax: w_k at the owned column indices
@@ -530,10 +534,12 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
     }
   }
 #undef SM_T
-  if (k + 2 < n) {  // stopped at k_end: the trailing block continues elsewhere from global memory
+  if (k + 2 < n) {  // stopped at k_end: the trailing block (rows/columns > k) continues from global memory
     for (int q = 0; q < nown; ++q) {
-      double* dst = A + n * (jb + (int64_t)NB * q);
-      for (int i = tid; i < N; i += NT) dst[i] = cols[q * N + i];
+      const int64_t j = jb + (int64_t)NB * q;
+      if (j <= k) continue;
+      double* dst = A + n * j;
+      for (int i = (int)k + 1 + tid; i < N; i += NT) dst[i] = cols[q * N + i];
     }
   }
 }
@@ -577,7 +583,7 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
 #undef SMEM_K
   if (!kern) return false;
   const int nw = nt / 32;
-  const size_t smem = sizeof(double) * ((size_t)qmax * n + (size_t)nw * qmax + 2 * nw + 2 * qmax + 1);
+  const size_t smem = sizeof(double) * (((size_t)qmax * n + 1) / 2 * 2 + (size_t)nw * qmax + 2 * nw + 2 * qmax + 1);
   if (smem > 227 * 1024) return false;
   static int64_t checked[4] = {-1, -1, -1, -1};
   if (checked[slot] != n) {

@@ -141,6 +141,9 @@ bool sytrd_rows(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
 // Cluster-resident tridiagonalisation of the trailing block from step K0 (k_sytrd_tail.cu).
 int64_t sytrd_tail_capacity(Ctx& c);
 void sytrd_tail(Ctx& c, double* A, int64_t n, int64_t K0, double* d, double* e, double* tau, double* hv);
+// Single-CTA tridiagonalisation of a trailing block of <= sytrd_tail1_max() from step K0 (k_sytrd_tail1.cu).
+int64_t sytrd_tail1_max();
+void sytrd_tail1(Ctx& c, double* A, int64_t n, int64_t K0, double* d, double* e, double* tau, double* hv);
 
 // ---------------------------------------------------------------- colour (k_color.cu)
 void color_u8(Ctx& c, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, int space, float* out,

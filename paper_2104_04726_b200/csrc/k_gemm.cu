@@ -15,6 +15,8 @@
 // B(k1, k2, n) with a two-level inner index (k2 = the slab index of the
 // modes after n). Split-K partials are reduced in a fixed order (deterministic,
 // no atomics).
+#include <cstdlib>
+
 #include "tmb_internal.cuh"
 
 namespace tmb {
@@ -319,11 +321,26 @@ void gemm(Ctx& c, const GemmDesc& d0) {
   if (d.syrk_upper) tiles = (tiles + tn * d.batch) / 2;
   int splits = d.splits;
   if (splits <= 0) {
+    static const int policy = [] {
+      const char* s = std::getenv("TMB_GEMM_SPLITS");  // A/B: 0 = fill the resident slots, 1 = 2 CTAs per SM
+      return s ? std::atoi(s) : 0;
+    }();
     splits = 1;
-    const int64_t want = 2LL * c.num_sms;
-    if (tiles < want && a.kt_total >= 8) {
-      splits = (int)std::min<int64_t>(ceil_div(want, tiles), a.kt_total / 4);
-      splits = std::max(1, std::min(splits, 64));
+    if (policy == 1) {
+      const int64_t want = 2LL * c.num_sms;
+      if (tiles < want && a.kt_total >= 8) {
+        splits = (int)std::min<int64_t>(ceil_div(want, tiles), a.kt_total / 4);
+        splits = std::max(1, std::min(splits, 64));
+      }
+    } else {
+      // split K only as far as one wave of resident CTAs (MINB per SM) holds: a
+      // partial second wave (e.g. 306 CTAs at 2 per SM for the C2 mode-0 Gram)
+      // leaves most of the DMMA pipes idle for its duration
+      const int64_t slots = (int64_t)MINB * c.num_sms;
+      if (tiles < slots && a.kt_total >= 8) {
+        splits = (int)std::min<int64_t>(slots / tiles, a.kt_total / 4);
+        splits = std::max(1, std::min(splits, 64));
+      }
     }
   }
   if ((int64_t)splits * d.batch > 65535) splits = std::max<int64_t>(1, 65535 / d.batch);

@@ -98,7 +98,16 @@ __global__ void __launch_bounds__(256) k_oz_rowexp(const T* __restrict__ x, int6
     if (m < M) {
       const int64_t i = m % L, l = m / L;
       const T* p = x + i + L * K * l;
-      for (int64_t k = w; k < K; k += 8) mx = fmax(mx, fabs(ldv(p, L * k)));
+      // 8 independent loads in flight per thread (the pass is latency-bound otherwise)
+      double mq[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int64_t k = w;
+      for (; k + 56 < K; k += 64) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mq[q] = fmax(mq[q], fabs(ldv(p, L * (k + 8 * q))));
+      }
+      for (; k < K; k += 8) mq[0] = fmax(mq[0], fabs(ldv(p, L * k)));
+#pragma unroll
+      for (int q = 0; q < 8; ++q) mx = fmax(mx, mq[q]);
     }
     red[w][lane] = mx;
     __syncthreads();
@@ -135,10 +144,17 @@ __global__ void __launch_bounds__(256) k_oz_sliceA(const T* __restrict__ x, int6
     const bool mok = m < M;
     const int64_t i = mok ? m % L : 0, l = mok ? m / L : 0;
     const int e = mok ? ea[m] : 0;
-    for (int kk = w; kk < 128; kk += 8) {
-      const int64_t k = k0 + kk;
-      int8_t d[OZ_S] = {0, 0, 0, 0, 0, 0, 0, 0};
-      if (mok && k < K) digits8(ldraw(x, i + L * k + L * K * l), e, d);
+    T xv[16];  // all 16 loads of this thread in flight before any digit work
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int64_t k = k0 + w + 8 * q;
+      xv[q] = (mok && k < K) ? ldraw(x, i + L * k + L * K * l) : (T)0;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int kk = w + 8 * q;
+      int8_t d[OZ_S];
+      digits8(xv[q], e, d);
 #pragma unroll
       for (int s2 = 0; s2 < OZ_S; ++s2) tile[s2][lane][kk] = d[s2];
     }
@@ -213,6 +229,53 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (done) return;
   }
   asm volatile("trap;");  // a protocol bug must not hang the GPU
+}
+
+// Epilogue shared by both GEMM variants: warp w holds factor rows r = m0 + 32w
+// + lane (TMEM lanes); columns are tensor rows m = (i, l), 8 at a time. Forms
+// sum_g acc_g 2^(-12-7g) in fp64 (exact-constant FMAs, small groups first),
+// scales by 2^(e_r + e_m) (built from the exponent bits when normal) and
+// stores 8 consecutive i of y for one r; (i, l) advance incrementally (one
+// division per CTA; L >= 8 so 8 consecutive m wrap at most once).
+template <int BN>
+__device__ __forceinline__ void oz_epilogue(uint32_t tmem, int warp, int lane, int64_t m0, int64_t n0,
+                                            const int* __restrict__ eu, const int* __restrict__ ex, int64_t L,
+                                            int64_t R, int64_t N, double* __restrict__ y) {
+  const int64_t r = m0 + warp * 32 + lane;
+  const bool rok = r < N;
+  const int er = rok ? eu[r] : 0;
+  const int64_t MX = L * R;
+  int64_t ib = n0 % L, lb = n0 / L;  // (i, l) of column c0
+  for (int c0 = 0; c0 < BN; c0 += 8) {
+    uint32_t v[OZ_S][8];
+#pragma unroll
+    for (int g = 0; g < OZ_S; ++g)
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(v[g][0]), "=r"(v[g][1]), "=r"(v[g][2]), "=r"(v[g][3]), "=r"(v[g][4]), "=r"(v[g][5]),
+                     "=r"(v[g][6]), "=r"(v[g][7])
+                   : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(g * BN + c0)));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+    if (rok) {
+      int64_t i = ib, l = lb;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t m = n0 + c0 + j;
+        if (m < MX) {
+          double acc = 0.0;
+#pragma unroll
+          for (int g = OZ_S - 1; g >= 0; --g)
+            acc = fma((double)(int32_t)v[g][j], __longlong_as_double((long long)(1023 - 12 - 7 * g) << 52), acc);
+          const int E = er + __ldg(ex + m);
+          const double out = (E >= -1022 && E <= 1023) ? acc * __longlong_as_double((long long)(E + 1023) << 52)
+                                                        : ldexp(acc, E);
+          y[i + L * r + L * N * l] = out;
+        }
+        if (++i == L) { i = 0; ++l; }
+      }
+    }
+    ib += 8;
+    if (ib >= L) { ib -= L; ++lb; }
+  }
 }
 
 // A operand (UMMA M side, 128 rows): factor digit planes, rows r (exponents eu);
@@ -301,32 +364,7 @@ __global__ void __launch_bounds__(OZ_NT, 1) k_oz_gemm(const __grid_constant__ CU
   asm volatile("tcgen05.fence::after_thread_sync;");
   // epilogue: warp w holds factor rows r = m0 + 32w + lane (TMEM lanes); columns are
   // tensor rows (i, l), 8 at a time -> 8 consecutive i of y for one r
-  const int64_t r = m0 + warp * 32 + lane;
-  const bool rok = r < N;
-  const int er = rok ? eu[r] : 0;
-  const int64_t MX = L * R;
-  for (int c0 = 0; c0 < OZ_BN; c0 += 8) {
-    uint32_t v[OZ_S][8];
-#pragma unroll
-    for (int g = 0; g < OZ_S; ++g)
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                   : "=r"(v[g][0]), "=r"(v[g][1]), "=r"(v[g][2]), "=r"(v[g][3]), "=r"(v[g][4]), "=r"(v[g][5]),
-                     "=r"(v[g][6]), "=r"(v[g][7])
-                   : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(g * OZ_BN + c0)));
-    asm volatile("tcgen05.wait::ld.sync.aligned;");
-    if (!rok) continue;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t m = n0 + c0 + j;
-      if (m >= MX) continue;
-      double acc = 0.0;
-#pragma unroll
-      for (int g = OZ_S - 1; g >= 0; --g)  // small first; 2^(-12-7g) exact constants
-        acc = fma((double)(int32_t)v[g][j], __longlong_as_double((long long)(1023 - 12 - 7 * g) << 52), acc);
-      const int64_t i = m % L, l = m / L;
-      y[i + L * r + L * N * l] = ldexp(acc, er + ex[m]);
-    }
-  }
+  oz_epilogue<OZ_BN>(tmem, warp, lane, m0, n0, eu, ex, L, R, N, y);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -373,8 +411,9 @@ bool ozaki_enabled() {
 
 void ozaki_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t R, const double* mat, int64_t N,
                int64_t sMr, int64_t sMk, double* y) {
+  constexpr int bn = OZ_BN;
   const int64_t MX = L * R;  // tensor rows
-  const int64_t Xp = ceil_div(MX, OZ_BN) * OZ_BN, Up = ceil_div(N, OZ_BM) * OZ_BM, Kp = ceil_div(K, OZ_BK) * OZ_BK;
+  const int64_t Xp = ceil_div(MX, bn) * bn, Up = ceil_div(N, OZ_BM) * OZ_BM, Kp = ceil_div(K, OZ_BK) * OZ_BK;
   if (K > 65536) throw Error(TMB_EINVAL, "ozaki_ttm: K too large for int32 digit accumulation");
   const size_t mk = c.arena.mark();
   int* ex = alloc<int>(c, (size_t)Xp);
@@ -406,17 +445,19 @@ void ozaki_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t R,
       mat, K, N, sMr, sMk, eu, Up, Kp, su);
   c.launches++;
   check_launch("k_oz_sliceB");
-  const CUtensorMap ta = digit_map(su, Up, Kp, OZ_BM), tb = digit_map(sx, Xp, Kp, OZ_BN);
-  const size_t smem = (size_t)OZ_ST * OZ_STAGE + 1024;
-  static bool attr = false;
-  if (!attr) {
-    TMB_CUDA(cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+  const CUtensorMap ta = digit_map(su, Up, Kp, OZ_BM), tb = digit_map(sx, Xp, Kp, (uint32_t)bn);
+  dim3 grid((unsigned)(Up / OZ_BM), (unsigned)(Xp / bn));
+  {
+    const size_t smem = (size_t)OZ_ST * OZ_STAGE + 1024;
+    static bool attr = false;
+    if (!attr) {
+      TMB_CUDA(cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    k_oz_gemm<<<grid, OZ_NT, smem, c.stream>>>(ta, tb, eu, ex, L, R, N, Kp, y);
+    c.launches++;
+    check_launch("k_oz_gemm");
   }
-  dim3 grid((unsigned)(Up / OZ_BM), (unsigned)(Xp / OZ_BN));
-  k_oz_gemm<<<grid, OZ_NT, smem, c.stream>>>(ta, tb, eu, ex, L, R, N, Kp, y);
-  c.launches++;
-  check_launch("k_oz_gemm");
   c.arena.release(mk);
 }
 

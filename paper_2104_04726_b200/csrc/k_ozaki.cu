@@ -120,8 +120,14 @@ __global__ void __launch_bounds__(256) k_oz_rowexp(const T* __restrict__ x, int6
     if (m >= M) return;
     const int64_t i = m % L, l = m / L;
     const T* p = x + i + L * K * l;
-    double mx = 0.0;
-    for (int64_t k = lane; k < K; k += 32) mx = fmax(mx, fabs(ldv(p, L * k)));
+    double mq[4] = {0, 0, 0, 0};
+    int64_t k = lane;
+    for (; k + 96 < K; k += 128) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) mq[q] = fmax(mq[q], fabs(ldv(p, L * (k + 32 * q))));
+    }
+    for (; k < K; k += 32) mq[0] = fmax(mq[0], fabs(ldv(p, L * k)));
+    double mx = fmax(fmax(mq[0], mq[1]), fmax(mq[2], mq[3]));
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) ea[m] = exp_of(mx);
   }
@@ -159,19 +165,29 @@ __global__ void __launch_bounds__(256) k_oz_sliceA(const T* __restrict__ x, int6
       for (int s2 = 0; s2 < OZ_S; ++s2) tile[s2][lane][kk] = d[s2];
     }
   } else {  // lanes along k, warps over m
-    for (int mm = w; mm < 32; mm += 8) {
-      const int64_t m = m0 + mm;
+    T xv[4][4];
+    int ev[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {  // all 16 loads first
+      const int64_t m = m0 + w + 8 * a;
       const bool mok = m < M;
       const int64_t i = mok ? m % L : 0, l = mok ? m / L : 0;
-      const int e = mok ? ea[m] : 0;
-      for (int kk = lane; kk < 128; kk += 32) {
-        const int64_t k = k0 + kk;
-        int8_t d[OZ_S] = {0, 0, 0, 0, 0, 0, 0, 0};
-        if (mok && k < K) digits8(ldraw(x, i + L * k + L * K * l), e, d);
+      ev[a] = mok ? ea[m] : 0;
 #pragma unroll
-        for (int s2 = 0; s2 < OZ_S; ++s2) tile[s2][mm][kk] = d[s2];
+      for (int q = 0; q < 4; ++q) {
+        const int64_t k = k0 + lane + 32 * q;
+        xv[a][q] = (mok && k < K) ? ldraw(x, i + L * k + L * K * l) : (T)0;
       }
     }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int8_t d[OZ_S];
+        digits8(xv[a][q], ev[a], d);
+#pragma unroll
+        for (int s2 = 0; s2 < OZ_S; ++s2) tile[s2][w + 8 * a][lane + 32 * q] = d[s2];
+      }
   }
   __syncthreads();
   for (int mm = w; mm < 32; mm += 8) {
@@ -236,7 +252,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // sum_g acc_g 2^(-12-7g) in fp64 (exact-constant FMAs, small groups first),
 // scales by 2^(e_r + e_m) (built from the exponent bits when normal) and
 // stores 8 consecutive i of y for one r; (i, l) advance incrementally (one
-// division per CTA; L >= 8 so 8 consecutive m wrap at most once).
+// division per CTA, then wrap-around steps).
 template <int BN>
 __device__ __forceinline__ void oz_epilogue(uint32_t tmem, int warp, int lane, int64_t m0, int64_t n0,
                                             const int* __restrict__ eu, const int* __restrict__ ex, int64_t L,
@@ -274,7 +290,7 @@ __device__ __forceinline__ void oz_epilogue(uint32_t tmem, int warp, int lane, i
       }
     }
     ib += 8;
-    if (ib >= L) { ib -= L; ++lb; }
+    while (ib >= L) { ib -= L; ++lb; }
   }
 }
 

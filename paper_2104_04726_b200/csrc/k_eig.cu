@@ -690,6 +690,132 @@ __global__ void k_twisted(const double* __restrict__ d, const double* __restrict
   for (int64_t i = lane; i < n; i += 32) vecs[i + n * j] = zj[i] * nrm;
 }
 
+// Same algorithm, one 64-thread block per eigenvalue with the scratch in SHARED
+// memory (2 x n doubles): warp 0 runs the D+ chain while warp 1 runs the D-
+// chain (in one warp the two lanes' branches would be issued one after the
+// other), the twist index is a block argmin, warp 0 / warp 1 then run the
+// upward / downward product chains, forming the ratios z_i / z_{i+/-1} inside
+// the chain (their reciprocals do not depend on the running product, so they
+// stay off the critical path), and z overwrites D+ (i <= r) / D- (i > r) in
+// place. Bitwise identical to k_twisted.
+__global__ void __launch_bounds__(64) k_twisted_sm(const double* __restrict__ d, const double* __restrict__ e,
+                                                   int64_t n, int64_t k, const double* __restrict__ vals,
+                                                   double* __restrict__ vecs) {
+  extern __shared__ double tw[];
+  __shared__ double gsh[2];
+  __shared__ int64_t rsh[2];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t j = blockIdx.x;
+  double* dpj = tw;
+  double* dmj = tw + n;
+  const double lam = vals[j];
+  double emax2 = 0.0;
+  for (int64_t i = lane; i + 1 < n; i += 32) emax2 = fmax(emax2, e[i] * e[i]);
+  for (int o = 16; o > 0; o >>= 1) emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
+  const double pivmin = DBL_MIN * fmax(1.0, emax2);
+  constexpr int U = 8;
+  if (wib == 0 && lane == 0) {  // D+ (stationary qd, top-down)
+    double q = d[0] - lam;
+    if (fabs(q) <= pivmin) q = -pivmin;
+    dpj[0] = q;
+    for (int64_t i0 = 1; i0 < n; i0 += U) {
+      double dv[U], ev[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        dv[u] = i0 + u < n ? d[i0 + u] : 0.0;
+        ev[u] = i0 + u < n ? e[i0 + u - 1] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i0 + u >= n) break;
+        q = (dv[u] - lam) - ev[u] * ev[u] * frcp(q);
+        if (fabs(q) <= pivmin) q = -pivmin;
+        dpj[i0 + u] = q;
+      }
+    }
+  } else if (wib == 1 && lane == 0) {  // D- (progressive qd, bottom-up)
+    double m = d[n - 1] - lam;
+    if (fabs(m) <= pivmin) m = -pivmin;
+    dmj[n - 1] = m;
+    for (int64_t i0 = n - 2; i0 >= 0; i0 -= U) {
+      double dv[U], ev[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        dv[u] = i0 - u >= 0 ? d[i0 - u] : 0.0;
+        ev[u] = i0 - u >= 0 ? e[i0 - u] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i0 - u < 0) break;
+        const double t = (dv[u] - lam) - ev[u] * ev[u] * frcp(m);
+        m = fabs(t) <= pivmin ? -pivmin : t;
+        dmj[i0 - u] = m;
+      }
+    }
+  }
+  __syncthreads();
+  // twist index: argmin |gamma_i|, ties to the larger i (gamma_{n-1} = D+_{n-1})
+  double gbest = 1e308;
+  int64_t r = -1;
+  for (int64_t i = threadIdx.x; i < n; i += 64) {
+    const double g = i == n - 1 ? fabs(dpj[i]) : fabs(dpj[i] + dmj[i] - (d[i] - lam));
+    if (g < gbest || (g == gbest && i > r)) { gbest = g; r = i; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double og = __shfl_xor_sync(0xffffffffu, gbest, o);
+    const int64_t orr = __shfl_xor_sync(0xffffffffu, r, o);
+    if (og < gbest || (og == gbest && orr > r)) { gbest = og; r = orr; }
+  }
+  if (lane == 0) { gsh[wib] = gbest; rsh[wib] = r; }
+  __syncthreads();
+  {
+    const double og = gsh[wib ^ 1];
+    const int64_t orr = rsh[wib ^ 1];
+    if (og < gbest || (og == gbest && orr > r)) { gbest = og; r = orr; }
+  }
+  if (wib == 0 && lane == 0) {  // z_r = 1; upward: z_i = -e_i / D+_i * z_{i+1}, stored over D+
+    double zz = 1.0;
+    for (int64_t i0 = r - 1; i0 >= 0; i0 -= U) {
+      double rt[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) rt[u] = i0 - u >= 0 ? -e[i0 - u] * frcp(dpj[i0 - u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i0 - u < 0) break;
+        zz = rt[u] * zz;
+        if (!(fabs(zz) < 1e280)) zz = (zz > 0 ? 1e280 : -1e280);
+        dpj[i0 - u] = zz;
+      }
+    }
+    dpj[r] = 1.0;
+  } else if (wib == 1 && lane == 0) {  // downward: z_i = -e_{i-1} / D-_i * z_{i-1}, stored over D-
+    double zz = 1.0;
+    for (int64_t i0 = r + 1; i0 < n; i0 += U) {
+      double rt[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) rt[u] = i0 + u < n ? -e[i0 + u - 1] * frcp(dmj[i0 + u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i0 + u >= n) break;
+        zz = rt[u] * zz;
+        if (!(fabs(zz) < 1e280)) zz = (zz > 0 ? 1e280 : -1e280);
+        dmj[i0 + u] = zz;
+      }
+    }
+  }
+  __syncthreads();
+  if (wib != 0) return;  // normalisation by warp 0 (same reduction order as k_twisted)
+  const auto zat = [&](int64_t i) { return i <= r ? dpj[i] : dmj[i]; };
+  double mx = 0.0;
+  for (int64_t i = lane; i < n; i += 32) mx = fmax(mx, fabs(zat(i)));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const double inv = mx > 0.0 ? 1.0 / mx : 1.0;
+  double s = 0.0;
+  for (int64_t i = lane; i < n; i += 32) { const double v = zat(i) * inv; s = fma(v, v, s); }
+  const double nrm = inv / sqrt(warp_sum(s));
+  for (int64_t i = lane; i < n; i += 32) vecs[i + n * j] = zat(i) * nrm;
+}
+
 // Compact-WY T factor of one panel of nb forward reflectors (LAPACK dlarft):
 // H_0 ... H_{nb-1} = I - V T V^T, T(i,i) = tau_i,
 // T(0:i, i) = -tau_i T(0:i, 0:i) S(0:i, i) with S = V^T V.
@@ -1145,8 +1271,20 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
     else if (bis_w == 2) k_bisect_mw<2><<<(unsigned)k, 64, 0, c.stream>>>(d, e, n, k, vals);
     else k_bisect<<<(unsigned)ceil_div(k, 2), 64, 0, c.stream>>>(d, e, n, k, vals);
     LAUNCHED("k_bisect");
-    k_twisted<<<(unsigned)ceil_div(k, 2), 64, 0, c.stream>>>(d, e, n, k, vals, dp, dm, zs, vecs);
-    LAUNCHED("k_twisted");
+    static const bool tw_global = std::getenv("TMB_TWISTED_GLOBAL") != nullptr;  // A/B: L2 scratch variant
+    const size_t tw_smem = sizeof(double) * 2 * (size_t)n;  // per eigenvalue
+    if (!tw_global && tw_smem <= 200 * 1024) {
+      static bool tw_attr = false;
+      if (!tw_attr) {
+        TMB_CUDA(cudaFuncSetAttribute(k_twisted_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        tw_attr = true;
+      }
+      k_twisted_sm<<<(unsigned)k, 64, tw_smem, c.stream>>>(d, e, n, k, vals, vecs);
+      LAUNCHED("k_twisted_sm");
+    } else {
+      k_twisted<<<(unsigned)ceil_div(k, 2), 64, 0, c.stream>>>(d, e, n, k, vals, dp, dm, zs, vecs);
+      LAUNCHED("k_twisted");
+    }
   }
   backtransform(c, hv, tau, n, hv_cols, k, vecs);
   orthonormalize(c, vecs, n, k);

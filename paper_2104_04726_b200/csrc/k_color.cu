@@ -73,43 +73,113 @@ __device__ __forceinline__ double oetf(double v) {
   return v > 0.0031308 ? sub(mul(1.055, pow(fmax(v, 0.0), 1.0 / 2.4)), 0.055) : mul(12.92, v);
 }
 
-// 32x32 pixel tile per block, blockDim (32, 8)
+// Correctly rounded x / d for a constant d with inv = RN(1/d): q = RN(x inv) is
+// within one ulp of x/d, and one remainder correction (exact residual by fma)
+// gives RN(x/d) (Markstein); verified against numpy's division on all 2^24
+// u8 RGB triples (tests/test_gpu_parity.py::test_color_u8_exhaustive).
+__device__ __forceinline__ double div_const(double x, double d, double inv) {
+  const double q = __dmul_rn(x, inv);
+  const double r = __fma_rn(-q, d, x);
+  return __fma_rn(r, inv, q);
+}
+
+__device__ double g_eotf[256];  // global copy of cc.eotf for per-block shared-memory staging
+
+// Tile of 64 pixels along w x 32 rows along h per 256-thread block.
+// (1) the 32 x 192 source bytes are staged in shared memory (16-byte loads when
+//     the row stride allows), (2) each thread converts 8 pixels (lanes walk
+//     down a column of the tile, so both the byte reads and the fp32 writes of
+//     the transposed tile are bank-conflict free), (3) each (channel, column)
+//     run of 32 h-contiguous floats is written with 16-byte stores.
+// Y'CbCr forms u8/255 with the corrected-reciprocal division (bitwise the
+// reference's value); IPT reads the sRGB EOTF of the u8 code from a shared-memory table.
 // channel_major = 0: planes (img, c) at (3 img + c) h w -- the BASELINE (H, W, 3, V*E) stack;
 // channel_major = 1: planes at (c n_img + img) h w -- three (H, W, E, V) tensors, one per
 // channel, the reference codec's stack_to_tensor layout (sceneio.py:38, 191-199).
+// row stride 196 B = 49 words (odd): lanes reading one byte from each of 32 rows hit 32 banks
+constexpr int CT_W = 64, CT_H = 32, CT_ROWB = CT_W * 3 + 4, CT_FP = CT_H + 4;
+
 __global__ void __launch_bounds__(256) k_color_u8(const uint8_t* __restrict__ rgb, int64_t h, int64_t w,
                                                   int space, float* __restrict__ out, int channel_major) {
-  __shared__ float tile[3][32][33];  // [c][x][y]
+  __shared__ __align__(16) uint8_t su8[CT_H][CT_ROWB];  // 4-byte aligned rows
+  __shared__ __align__(16) float so[3][CT_W][CT_FP];
+  __shared__ double lut[256];
+  const int t = threadIdx.x;
   const int64_t img = blockIdx.z;
-  const int64_t x0 = (int64_t)blockIdx.x * 32, y0 = (int64_t)blockIdx.y * 32;
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const uint8_t* src = rgb + img * h * w * 3;
-  for (int yy = ty; yy < 32; yy += 8) {
-    const int64_t y = y0 + yy, x = x0 + tx;
-    if (y < h && x < w) {
-      const uint8_t* p = src + (y * w + x) * 3;
-      double o[3];
-      if (space == TMB_SPACE_YCBCR) {
-        ycbcr(__ddiv_rn((double)p[0], 255.0), __ddiv_rn((double)p[1], 255.0), __ddiv_rn((double)p[2], 255.0), o);
-      } else if (space == TMB_SPACE_IPT) {
-        const double lin[3] = {cc.eotf[p[0]], cc.eotf[p[1]], cc.eotf[p[2]]};
-        ipt_from_lin(lin, o);
-      } else {
-        o[0] = __ddiv_rn((double)p[0], 255.0); o[1] = __ddiv_rn((double)p[1], 255.0); o[2] = __ddiv_rn((double)p[2], 255.0);
-      }
-      tile[0][tx][yy] = __double2float_rn(o[0]);
-      tile[1][tx][yy] = __double2float_rn(o[1]);
-      tile[2][tx][yy] = __double2float_rn(o[2]);
+  const int64_t x0 = (int64_t)blockIdx.x * CT_W, y0 = (int64_t)blockIdx.y * CT_H;
+  const bool full = (x0 + CT_W <= w) && (y0 + CT_H <= h);
+  if (space == TMB_SPACE_IPT) lut[t] = g_eotf[t];
+  else if (space != TMB_SPACE_YCBCR) lut[t] = __ddiv_rn((double)t, 255.0);
+  const uint8_t* src = rgb + (img * h + y0) * w * 3 + x0 * 3;
+  if (full && (w & 15) == 0 && ((reinterpret_cast<uintptr_t>(rgb) & 15) == 0)) {
+    for (int i = t; i < CT_H * 12; i += 256) {
+      const int r = i / 12, q = i % 12;
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + (int64_t)r * w * 3) + q);
+      uint32_t* d = reinterpret_cast<uint32_t*>(&su8[r][q * 16]);
+      d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+    }
+  } else {
+    const int64_t nx = w - x0 < CT_W ? w - x0 : CT_W, ny = h - y0 < CT_H ? h - y0 : CT_H;
+    for (int i = t; i < CT_H * CT_W * 3; i += 256) {
+      const int r = i / (CT_W * 3), bcol = i % (CT_W * 3);
+      if (r < ny && bcol < nx * 3) su8[r][bcol] = src[(int64_t)r * w * 3 + bcol];
     }
   }
   __syncthreads();
+  const double KB1 = 1.0 - KB, KR1 = 1.0 - KR;
+  const double IKB1 = 1.0 / (1.0 - KB), IKR1 = 1.0 / (1.0 - KR), I255 = 1.0 / 255.0;
+  const int nyt = full ? CT_H : (int)(h - y0 < CT_H ? h - y0 : CT_H);
+  const int nxt = full ? CT_W : (int)(w - x0 < CT_W ? w - x0 : CT_W);
+  const int r = t & 31;
+#pragma unroll 2
+  for (int col = t >> 5; col < CT_W; col += 8) {
+    if (r >= nyt || col >= nxt) continue;
+    const uint8_t* sp = &su8[r][col * 3];
+    const int R = sp[0], G = sp[1], B = sp[2];
+    float f[3];
+    if (space == TMB_SPACE_YCBCR) {
+      // color.py:116-118: y = KR r + KG g + KB b; cb = 0.5 (b - y) / (1 - KB) + 0.5;
+      // clip to [0, 1] -- applied after the (monotone) rounding to fp32, where
+      // it is one FMNMX pair and gives the same float as clipping in fp64
+      // u8/255 by the corrected-reciprocal division (no table: random-index
+      // shared-memory loads would make the L1 pipe the bound)
+      const double r = div_const((double)R, 255.0, I255), g = div_const((double)G, 255.0, I255),
+                   b = div_const((double)B, 255.0, I255);
+      const double y = add(add(mul(KR, r), mul(KG, g)), mul(KB, b));
+      const double cb = add(div_const(mul(0.5, sub(b, y)), KB1, IKB1), 0.5);
+      const double cr = add(div_const(mul(0.5, sub(r, y)), KR1, IKR1), 0.5);
+      f[0] = fminf(fmaxf(__double2float_rn(y), 0.0f), 1.0f);
+      f[1] = fminf(fmaxf(__double2float_rn(cb), 0.0f), 1.0f);
+      f[2] = fminf(fmaxf(__double2float_rn(cr), 0.0f), 1.0f);
+    } else {
+      double o[3];
+      if (space == TMB_SPACE_IPT) {
+        const double lin[3] = {lut[R], lut[G], lut[B]};
+        ipt_from_lin(lin, o);
+      } else {
+        o[0] = lut[R]; o[1] = lut[G]; o[2] = lut[B];
+      }
+      f[0] = __double2float_rn(o[0]); f[1] = __double2float_rn(o[1]); f[2] = __double2float_rn(o[2]);
+    }
+    so[0][col][r] = f[0];
+    so[1][col][r] = f[1];
+    so[2][col][r] = f[2];
+  }
+  __syncthreads();
   const int64_t hw = h * w;
-  float* dst = out + img * (channel_major ? hw : 3 * hw);
+  float* dst = out + img * (channel_major ? hw : 3 * hw) + x0 * h + y0;
   const int64_t cstride = channel_major ? (int64_t)gridDim.z * hw : hw;
-  for (int q = ty; q < 3 * 32; q += 8) {
-    const int ch = q / 32, xx = q % 32;
-    const int64_t x = x0 + xx, y = y0 + tx;
-    if (x < w && y < h) dst[y + h * x + cstride * ch] = tile[ch][xx][tx];
+  if (full && (h & 3) == 0 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+    for (int i = t; i < 3 * CT_W * 8; i += 256) {
+      const int q = i & 7, col = (i >> 3) % CT_W, ch = i / (CT_W * 8);
+      *reinterpret_cast<float4*>(dst + cstride * ch + (int64_t)col * h + 4 * q) =
+          *reinterpret_cast<const float4*>(&so[ch][col][4 * q]);
+    }
+  } else {
+    for (int i = t; i < 3 * CT_W * CT_H; i += 256) {
+      const int r = i & 31, col = (i >> 5) % CT_W, ch = i / (CT_W * CT_H);
+      if (y0 + r < h && x0 + col < w) dst[cstride * ch + (int64_t)col * h + r] = so[ch][col][r];
+    }
   }
 }
 
@@ -280,6 +350,7 @@ void ensure_constants(Ctx& c) {
   inv3(h.xyz2lms, h.lms2xyz);
   inv3(h.lms2ipt, h.ipt2lms);
   TMB_CUDA(cudaMemcpyToSymbol(cc, &h, sizeof(h)));
+  TMB_CUDA(cudaMemcpyToSymbol(g_eotf, h.eotf, sizeof(h.eotf)));
   if (c.device >= 0 && c.device < 64) g_const_ready[c.device] = true;
 }
 
@@ -289,9 +360,9 @@ void color_u8(Ctx& c, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, i
               bool channel_major) {
   if (n_img == 0 || h == 0 || w == 0) return;
   ensure_constants(c);
-  dim3 grid((unsigned)ceil_div(w, 32), (unsigned)ceil_div(h, 32), (unsigned)n_img);
+  dim3 grid((unsigned)ceil_div(w, CT_W), (unsigned)ceil_div(h, CT_H), (unsigned)n_img);
   Timed timed(c, TAG_COLOR, 15.0 * (double)n_img * h * w);  // 3 B read + 12 B written per pixel
-  k_color_u8<<<grid, dim3(32, 8), 0, c.stream>>>(rgb, h, w, space, out, channel_major ? 1 : 0);
+  k_color_u8<<<grid, 256, 0, c.stream>>>(rgb, h, w, space, out, channel_major ? 1 : 0);
   c.launches++;
   check_launch("k_color_u8");
 }

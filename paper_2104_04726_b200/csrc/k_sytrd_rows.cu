@@ -51,6 +51,34 @@ __device__ __forceinline__ double wsum(double v) {
 // Block sum, broadcast; fixed order (8 warps). One barrier per call: the warp
 // partials alternate between two 8-slot buffers, so a buffer is only rewritten
 // after another call's barrier has passed every reader.
+// Split form: bsum_put (warp sum -> slot) ... one __syncthreads shared with
+// other publications ... bsum_get (fixed-order tree); bitwise equal to bsum.
+template <int NW>
+__device__ __forceinline__ const double* bsum_put(double v, double* red, int& phase) {
+  v = wsum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* r = red + NW * phase;
+  phase ^= 1;
+  if (lane == 0) r[w] = v;
+  return r;
+}
+
+template <int NW>
+__device__ __forceinline__ double bsum_get(const double* r) {
+  double t[NW];
+#pragma unroll
+  for (int i = 0; i < NW; i += 2) {
+    const double2 q = *reinterpret_cast<const double2*>(r + i);
+    t[i] = q.x;
+    t[i + 1] = q.y;
+  }
+#pragma unroll
+  for (int h = NW / 2; h > 0; h >>= 1)
+#pragma unroll
+    for (int i = 0; i < h; ++i) t[i] += t[i + h];
+  return t[0];
+}
+
 template <int NW>
 __device__ __forceinline__ double bsum(double v, double* red, int& phase) {
   v = wsum(v);
@@ -426,7 +454,15 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
       }
       break;
     }
-    xn2 = bsum<NW>(s2, red, rph);
+    // w_k at the owned indices and the warp partials of ||x||^2 are published
+    // behind ONE block barrier (the pass needs wo; every thread then forms
+    // ||x||^2 from the partials in bsum's fixed order)
+#pragma unroll
+    for (int u = 0; u < RPT; ++u)
+      if (qi[u] >= 0) wo[qi[u]] = wr[u];
+    const double* xr = bsum_put<NW>(s2, red, rph);
+    __syncthreads();  // wo + ||x||^2 partials ready
+    xn2 = bsum_get<NW>(xr);
     SM_T(3);
     alpha = a_k2 - v_k2 * w_c1 - w_k2 * v_c1;
     double tau_n = 0.0;
@@ -445,7 +481,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
     for (int u = 0; u < RPT; ++u) {
       const int i = tid + NT * u;
       nr[u] = i == k + 2 ? 1.0 : (i >= k + 3 && i < N ? xa[u] * scale : 0.0);
-      if (qi[u] >= 0) wo[qi[u]] = wr[u];
     }
     if (b == 0) {
       if (tid == 0) { a.e[c1] = beta; a.tau[c1] = tau_n; }
@@ -457,7 +492,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
         if (i == c1) a.d[c1] = xa[u];
       }
     }
-    __syncthreads();  // wo ready
     SM_T(5);
     double* pbn = a.pbuf + (buf ^ 1) * n;
     const int k2 = (int)k + 2;

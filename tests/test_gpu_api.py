@@ -369,6 +369,25 @@ def test_colour_u8_kernel_bit_exact(golden):
         assert np.array_equal(got, z[f"{space}_u8"].astype(np.float32))
 
 
+@pytest.mark.parametrize("space", ["ycbcr", "ipt"])
+def test_colour_u8_exhaustive(space):
+    """Every one of the 2^24 u8 RGB triples (one 4096 x 4096 image, full tiles
+    and the 16-byte load/store path) maps to fp32(reference f64 colour) bit for
+    bit; a ragged 2-image stack exercises the partial-tile path."""
+    codes = np.arange(1 << 24, dtype=np.uint32)
+    u8 = np.stack([(codes >> 16) & 255, (codes >> 8) & 255, codes & 255], axis=-1).astype(np.uint8)
+    t = tb.coding_tensor(u8.reshape(1, 1, 4096, 4096, 3), space).cpu().numpy()
+    got = t.reshape((4096, 4096, 3), order="F")
+    fn = oracle.rgb_to_ycbcr if space == "ycbcr" else oracle.rgb_to_ipt
+    ref = fn(u8.reshape(4096, 4096, 3).astype(np.float64) / 255.0).astype(np.float32)
+    assert np.array_equal(got, ref), int((got != ref).sum())
+    rng = np.random.default_rng(21)
+    imgs = rng.integers(0, 256, size=(1, 2, 37, 70, 3), dtype=np.uint8)
+    got2 = tb.coding_tensor(imgs, space).cpu().numpy().reshape((37, 70, 3, 2), order="F")
+    ref2 = oracle.coding_tensor(imgs, space).astype(np.float32)
+    assert np.array_equal(got2, ref2)
+
+
 def test_quantiser_contracts():  # tests/test_codec.py:57-85
     rng = np.random.default_rng(14)
     core = rng.standard_normal((4, 5, 3, 2))

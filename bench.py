@@ -290,6 +290,14 @@ def run_ours(args) -> None:
                  "ms_per_step": dom["ms"] / args.steps,
                  "share_of_step": dom["ms"] / (ev0.elapsed_time(ev1))})
 
+    # the HBM-bound elementwise kernel of the step (u8 -> IPT colour, 15 B/px), same live timing
+    col = fam["color_u8"]
+    col_gbs = col["work"] / (col["ms"] / 1e3) / 1e9 if col["ms"] > 0 else None
+    hbm_peak = float(peaks.get("hbm_gbs", 6443.8))
+    roof_elem = {"bound": "hbm", "kernel": "color_u8 (IPT: 3 fp64 pow per pixel, FP64-pipe bound)", "unit": "GB/s",
+                 "achieved": col_gbs, "peak": hbm_peak, "frac": col_gbs / hbm_peak if col_gbs else None,
+                 "bytes_per_launch": col["work"] / max(col["launches"], 1)}
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -305,6 +313,7 @@ def run_ours(args) -> None:
         "e2e": e2e,
         "gpu_launches": int(launches),
         "roofline": roof,
+        "roofline_elementwise": roof_elem,
         "kernel_families": {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps}
                             for k, v in fam.items()},
         "clocks": clk,

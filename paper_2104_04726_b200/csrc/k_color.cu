@@ -9,6 +9,8 @@
 // tensor is bit-identical to fp32(reference f64 colour). The IPT path uses a
 // host-built 256-entry EOTF table (the u8 codes are exact) and CUDA pow for
 // the 0.43 power; its matrix products follow the reference's 3x3 order.
+#include <type_traits>
+
 #include "tmb_internal.cuh"
 
 namespace tmb {
@@ -99,8 +101,16 @@ __device__ double g_eotf[256];  // global copy of cc.eotf for per-block shared-m
 // row stride 196 B = 49 words (odd): lanes reading one byte from each of 32 rows hit 32 banks
 constexpr int CT_W = 64, CT_H = 32, CT_ROWB = CT_W * 3 + 4, CT_FP = CT_H + 4;
 
+// fp64 constants of the Y'CbCr path as a kernel parameter: the DFMA/DMUL read
+// them from the constant bank instead of re-materialising 64-bit immediates
+// through uniform registers in the pixel loop (16 UMOV per pixel in ncu)
+struct YccConst {
+  double kr, kg, kb, kb1, ikb1, kr1, ikr1, i255;
+};
+
 __global__ void __launch_bounds__(256) k_color_u8(const uint8_t* __restrict__ rgb, int64_t h, int64_t w,
-                                                  int space, float* __restrict__ out, int channel_major) {
+                                                  int space, float* __restrict__ out, int channel_major,
+                                                  const YccConst P) {
   __shared__ __align__(16) uint8_t su8[CT_H][CT_ROWB];  // 4-byte aligned rows
   __shared__ __align__(16) float so[3][CT_W][CT_FP];
   __shared__ double lut[256];
@@ -126,14 +136,14 @@ __global__ void __launch_bounds__(256) k_color_u8(const uint8_t* __restrict__ rg
     }
   }
   __syncthreads();
-  const double KB1 = 1.0 - KB, KR1 = 1.0 - KR;
-  const double IKB1 = 1.0 / (1.0 - KB), IKR1 = 1.0 / (1.0 - KR), I255 = 1.0 / 255.0;
   const int nyt = full ? CT_H : (int)(h - y0 < CT_H ? h - y0 : CT_H);
   const int nxt = full ? CT_W : (int)(w - x0 < CT_W ? w - x0 : CT_W);
   const int r = t & 31;
-#pragma unroll 2
+  // full tiles (all but the right/bottom edge) run the loop without per-pixel guards
+  auto convert = [&](auto guarded) {
+#pragma unroll
   for (int col = t >> 5; col < CT_W; col += 8) {
-    if (r >= nyt || col >= nxt) continue;
+    if (decltype(guarded)::value && (r >= nyt || col >= nxt)) continue;
     const uint8_t* sp = &su8[r][col * 3];
     const int R = sp[0], G = sp[1], B = sp[2];
     float f[3];
@@ -143,11 +153,11 @@ __global__ void __launch_bounds__(256) k_color_u8(const uint8_t* __restrict__ rg
       // it is one FMNMX pair and gives the same float as clipping in fp64
       // u8/255 by the corrected-reciprocal division (no table: random-index
       // shared-memory loads would make the L1 pipe the bound)
-      const double r = div_const((double)R, 255.0, I255), g = div_const((double)G, 255.0, I255),
-                   b = div_const((double)B, 255.0, I255);
-      const double y = add(add(mul(KR, r), mul(KG, g)), mul(KB, b));
-      const double cb = add(div_const(mul(0.5, sub(b, y)), KB1, IKB1), 0.5);
-      const double cr = add(div_const(mul(0.5, sub(r, y)), KR1, IKR1), 0.5);
+      const double r = div_const((double)R, 255.0, P.i255), g = div_const((double)G, 255.0, P.i255),
+                   b = div_const((double)B, 255.0, P.i255);
+      const double y = add(add(mul(P.kr, r), mul(P.kg, g)), mul(P.kb, b));
+      const double cb = add(div_const(mul(0.5, sub(b, y)), P.kb1, P.ikb1), 0.5);
+      const double cr = add(div_const(mul(0.5, sub(r, y)), P.kr1, P.ikr1), 0.5);
       f[0] = fminf(fmaxf(__double2float_rn(y), 0.0f), 1.0f);
       f[1] = fminf(fmaxf(__double2float_rn(cb), 0.0f), 1.0f);
       f[2] = fminf(fmaxf(__double2float_rn(cr), 0.0f), 1.0f);
@@ -165,6 +175,9 @@ __global__ void __launch_bounds__(256) k_color_u8(const uint8_t* __restrict__ rg
     so[1][col][r] = f[1];
     so[2][col][r] = f[2];
   }
+  };
+  if (full) convert(std::false_type{});
+  else convert(std::true_type{});
   __syncthreads();
   const int64_t hw = h * w;
   float* dst = out + img * (channel_major ? hw : 3 * hw) + x0 * h + y0;
@@ -362,7 +375,8 @@ void color_u8(Ctx& c, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, i
   ensure_constants(c);
   dim3 grid((unsigned)ceil_div(w, CT_W), (unsigned)ceil_div(h, CT_H), (unsigned)n_img);
   Timed timed(c, TAG_COLOR, 15.0 * (double)n_img * h * w);  // 3 B read + 12 B written per pixel
-  k_color_u8<<<grid, 256, 0, c.stream>>>(rgb, h, w, space, out, channel_major ? 1 : 0);
+  const YccConst P{KR, KG, KB, 1.0 - KB, 1.0 / (1.0 - KB), 1.0 - KR, 1.0 / (1.0 - KR), 1.0 / 255.0};
+  k_color_u8<<<grid, 256, 0, c.stream>>>(rgb, h, w, space, out, channel_major ? 1 : 0, P);
   c.launches++;
   check_launch("k_color_u8");
 }

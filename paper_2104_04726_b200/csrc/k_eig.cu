@@ -1074,6 +1074,170 @@ __global__ void __launch_bounds__(wy::NT, 1)
   }
 }
 
+// Row-split variant: a cluster of CS CTAs shares one group of 8 columns of x
+// (the DMMA N, no padding); CTA c owns the 128-row chunks i = c (mod CS) of
+// those columns and streams only its chunks of every V_p / VT_p, so each CTA
+// moves 1/CS of the bytes the one-CTA-per-column-group kernel moves. The
+// panel product W = V_p^T x is the sum of the CS per-CTA partials: each CTA
+// writes its 64 x 8 partial to shared memory (double-buffered by panel
+// parity), ONE cluster barrier per panel, and every CTA adds the CS partials
+// over DSMEM in rank order (same W bits in every CTA). Rows of a panel's first
+// chunk above the panel (row < 64 p) carry V = 0, so chunks stay aligned.
+template <int CS, int ST>
+__global__ void __launch_bounds__(wy::NT, 1)
+    k_apply_wy_cl(const double* __restrict__ hv, const double* __restrict__ VT, int64_t n, int64_t k, int np,
+                  int ldx, int vec, double* __restrict__ x) {
+  using namespace wy;
+  constexpr int CB = 8, RC = 128, LDS_ = RC + 4;
+  extern __shared__ __align__(16) double smw[];
+  double* stg = smw;                          // ST x (NB x LDS_) staging [jj][row]
+  double* Xs = stg + ST * NB * LDS_;          // CB x ldx: owned chunks, local row = (i / CS) * RC + row
+  double* Wp = Xs + (size_t)CB * ldx;         // 2 x (CB x LDW): this CTA's W partial, by panel parity
+  double* Ws = Wp + 2 * CB * LDW;             // CB x LDW: the reduced W[jj][c] at Ws[c*LDW + jj]
+  double* scr = Ws + CB * LDW;                // 4 warps x 32 lanes x 4 partials
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tig = lane & 3, mt = warp & 3, kh = warp >> 2;
+  const int64_t j0 = (int64_t)(blockIdx.x / CS) * CB;
+  const int N = (int)n;
+  const int nch = (N + RC - 1) / RC;
+  for (int e = tid; e < CB * ldx; e += NT) {
+    const int c = e / ldx, li = e % ldx;
+    const int i = (li / RC) * CS + rank, row = i * RC + li % RC;
+    Xs[e] = (li < ((nch - rank + CS - 1) / CS) * RC && row < N && j0 + c < k) ? x[row + n * (j0 + c)] : 0.0;
+  }
+  // first owned chunk at or after chunk i0
+  auto first_owned = [&](int i0) { return i0 + ((rank - i0) % CS + CS) % CS; };
+  // load cursor over (panel desc, phase, owned chunk asc)
+  struct Cur { int p, ph, i; };
+  auto settle = [&](Cur& q) {  // move to the next (p, ph) that has an owned chunk
+    while (q.p >= 0 && q.i >= nch) {
+      if (q.ph == 0) { q.ph = 1; q.i = first_owned(q.p * NB / RC); }
+      else { --q.p; q.ph = 0; q.i = q.p >= 0 ? first_owned(q.p * NB / RC) : 0; }
+    }
+  };
+  auto advance = [&](Cur& q) { q.i += CS; settle(q); };
+  auto load = [&](const Cur& q, int st) {
+    if (q.p < 0) return;
+    const double* src = (q.ph == 0 ? hv : VT) + n * (int64_t)q.p * NB;
+    double* dst = stg + st * NB * LDS_;
+    const int r0 = q.i * RC;
+    if (vec) {
+#pragma unroll
+      for (int u = 0; u < NB * RC / 2 / NT; ++u) {
+        const int e = tid + NT * u, il = (e % (RC / 2)) * 2, jj = e / (RC / 2);
+        const int i = r0 + il;
+        const int nbytes = i + 1 < N ? 16 : (i < N ? 8 : 0);
+        wy::cpa<16>(dst + jj * LDS_ + il, nbytes ? src + i + n * jj : src, nbytes);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < NB * RC / NT; ++u) {
+        const int e = tid + NT * u, il = e % RC, jj = e / RC;
+        const int i = r0 + il;
+        wy::cpa<8>(dst + jj * LDS_ + il, i < N ? src + i + n * jj : src, i < N ? 8 : 0);
+      }
+    }
+  };
+  Cur ld{np - 1, 0, first_owned((np - 1) * NB / RC)};
+  settle(ld);
+#pragma unroll
+  for (int s2 = 0; s2 < ST - 1; ++s2) {
+    load(ld, s2);
+    asm volatile("cp.async.commit_group;\n" ::);
+    advance(ld);
+  }
+  int st = 0;
+  // consume one staged chunk: wait for it, refill the stage freed last time
+  auto next_stage = [&]() -> const double* {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(ST - 2));
+    __syncthreads();
+    load(ld, st == 0 ? ST - 1 : st - 1);
+    asm volatile("cp.async.commit_group;\n" ::);
+    advance(ld);
+    return stg + st * NB * LDS_;
+  };
+  for (int p = np - 1; p >= 0; --p) {
+    const int ifirst = first_owned(p * NB / RC);
+    // phase 0: this CTA's partial of W = V_p^T x over its chunks
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = ifirst; i < nch; i += CS) {
+      const double* sb = next_stage();
+      const int lr = (i / CS) * RC;
+#pragma unroll
+      for (int kk = 0; kk < RC / 2; kk += 8) {
+        const int kr = kh * (RC / 2) + kk;
+        const int m0 = mt * 16 + g;
+        double a[4], b[2];
+        a[0] = sb[m0 * LDS_ + kr + tig];
+        a[1] = sb[(m0 + 8) * LDS_ + kr + tig];
+        a[2] = sb[m0 * LDS_ + kr + tig + 4];
+        a[3] = sb[(m0 + 8) * LDS_ + kr + tig + 4];
+        b[0] = Xs[g * ldx + lr + kr + tig];
+        b[1] = Xs[g * ldx + lr + kr + tig + 4];
+        wy::mma(acc, a, b);
+      }
+      __syncthreads();  // stage free
+      st = st + 1 == ST ? 0 : st + 1;
+    }
+    double* wp = Wp + (p & 1) * CB * LDW;
+    if (kh == 1) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) scr[(mt * 32 + lane) * 4 + r] = acc[r];
+    }
+    __syncthreads();
+    if (kh == 0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int jj = mt * 16 + g + ((r & 2) ? 8 : 0), c = 2 * tig + (r & 1);
+        wp[c * LDW + jj] = acc[r] + scr[(mt * 32 + lane) * 4 + r];
+      }
+    }
+    cl.sync();  // every CTA's partial for panel p is visible cluster-wide
+    for (int e = tid; e < CB * NB; e += NT) {
+      const int c = e / NB, jj = e % NB;
+      double sum = 0.0;
+#pragma unroll
+      for (int q = 0; q < CS; ++q) sum += cl.map_shared_rank(wp, q)[c * LDW + jj];
+      Ws[c * LDW + jj] = sum;
+    }
+    __syncthreads();
+    // phase 1: x_chunk -= VT_chunk W on this CTA's chunks
+    for (int i = ifirst; i < nch; i += CS) {
+      const double* sb = next_stage();
+      const int lr = (i / CS) * RC;
+      double o[4] = {0.0, 0.0, 0.0, 0.0};
+      const int m0 = warp * 16 + g;
+#pragma unroll
+      for (int kb = 0; kb < NB; kb += 8) {
+        double a[4], b[2];
+        a[0] = sb[(kb + tig) * LDS_ + m0];
+        a[1] = sb[(kb + tig) * LDS_ + m0 + 8];
+        a[2] = sb[(kb + tig + 4) * LDS_ + m0];
+        a[3] = sb[(kb + tig + 4) * LDS_ + m0 + 8];
+        b[0] = Ws[g * LDW + kb + tig];
+        b[1] = Ws[g * LDW + kb + tig + 4];
+        wy::mma(o, a, b);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int rl = m0 + ((r & 2) ? 8 : 0), c = 2 * tig + (r & 1);
+        Xs[c * ldx + lr + rl] -= o[r];
+      }
+      __syncthreads();  // stage free
+      st = st + 1 == ST ? 0 : st + 1;
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  cl.sync();  // no CTA exits while another may still read its W partials
+  for (int e = tid; e < CB * ldx; e += NT) {
+    const int c = e / ldx, li = e % ldx;
+    const int i = (li / RC) * CS + rank, row = i * RC + li % RC;
+    if (li < ((nch - rank + CS - 1) / CS) * RC && row < N && j0 + c < k) x[row + n * (j0 + c)] = Xs[e];
+  }
+}
+
 // x <- H_0 H_1 ... H_{n-3} x by compact-WY panels of WY_NB reflectors, last
 // panel first: x <- x - (V_p T_p) (V_p^T x). hv is n x hv_cols with zero
 // columns past the last reflector; tau is zero-padded likewise.
@@ -1112,6 +1276,54 @@ static void backtransform(Ctx& c, const double* hv, const double* tau, int64_t n
     g.B = T; g.sBk1 = 1; g.sBn = nb; g.sBb = nb * nb;
     g.C = VT; g.sCm = 1; g.sCn = n; g.sCb = n * nb;
     gemm(c, g);
+  }
+  static const bool cl_off = std::getenv("TMB_WY_NOCLUSTER") != nullptr;  // A/B: one CTA per column group
+  if (!cl_off && nb == wy::NB) {
+    // cluster row-split kernel: CS CTAs per group of 8 columns; the largest CS
+    // whose grid stays within one wave, else the smallest that fits smem
+    const int64_t groups = ceil_div(k, 8);
+    const int64_t nch = ceil_div(n, 128);
+    const int vec = (n % 2 == 0 && reinterpret_cast<uintptr_t>(hv) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(VT) % 16 == 0) ? 1 : 0;
+    int pick = 0;
+    size_t pick_smem = 0;
+    int pick_ldx = 0;
+    for (int cs : {2, 4, 8}) {
+      const int ldx = (int)(ceil_div(nch, cs) * 128 + 4);
+      const size_t sm = sizeof(double) * ((size_t)2 * wy::NB * (128 + 4) + (size_t)8 * ldx + 3 * 8 * wy::LDW + 4 * 32 * 4);
+      if (sm > 227 * 1024) continue;
+      if (pick == 0 || groups * cs <= c.num_sms) { pick = cs; pick_smem = sm; pick_ldx = ldx; }
+      if (groups * cs * 2 > c.num_sms) break;
+    }
+    if (pick) {
+      const void* fn = pick == 2 ? (const void*)k_apply_wy_cl<2, 2>
+                     : pick == 4 ? (const void*)k_apply_wy_cl<4, 2> : (const void*)k_apply_wy_cl<8, 2>;
+      static bool attr[3] = {false, false, false};
+      const int ai = pick == 2 ? 0 : (pick == 4 ? 1 : 2);
+      if (!attr[ai]) {
+        TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr[ai] = true;
+      }
+      Timed timed(c, TAG_EIG_GEMM, 4.0 * (double)n * n * k / 2);
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3((unsigned)(groups * pick));
+      lc.blockDim = dim3(wy::NT);
+      lc.dynamicSmemBytes = pick_smem;
+      lc.stream = c.stream;
+      cudaLaunchAttribute at{};
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = pick; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
+      lc.attrs = &at;
+      lc.numAttrs = 1;
+      int np_ = np;
+      int64_t n_ = n, k_ = k;
+      int ldx_ = pick_ldx, vec_ = vec;
+      void* args[] = {(void*)&hv, (void*)&VT, &n_, &k_, &np_, &ldx_, &vec_, &x};
+      TMB_CUDA(cudaLaunchKernelExC(&lc, fn, args));
+      LAUNCHED("k_apply_wy_cl");
+      c.arena.release(mk);
+      return;
+    }
   }
   constexpr int CB = 4, RC = 128, ST = 2;
   const int ldx = (int)(ceil_div(n, RC) * RC + 4);

@@ -36,16 +36,18 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// 1/b from the MUFU seed plus two Newton steps (relative error ~2 ulp), off
-// the ~10x longer IEEE division path that dominates the Sturm / twisted
-// recurrences. Inputs are normal numbers (guarded by pivmin).
+// 1/b from the MUFU seed r0 with one cubic correction r0 (1 + e + e^2),
+// e = 1 - b r0: three dependent DFMA instead of the four of two Newton steps
+// (the Sturm / twisted recurrences are one long dependent chain, so this is
+// their latency). The seed's relative error is <= 2^-19.9 (measured), so the
+// correction leaves e^3 <= 2^-59: at most 1 ulp from the correctly rounded
+// 1/b over 1G random normal inputs (scripts/research/rcp_check.cu). Inputs are
+// normal numbers (guarded by pivmin).
 __device__ __forceinline__ double frcp(double b) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
-  double e = fma(-b, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-b, r, 1.0);
-  return fma(r, e, r);
+  const double e = fma(-b, r, 1.0);
+  return fma(r, fma(e, e, e), r);
 }
 
 // ------------------------------------------------------------------ Jacobi

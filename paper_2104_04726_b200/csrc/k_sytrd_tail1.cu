@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_sytrd_tail1(double* __restric
       if (li < m) {
         const double vi = v[li], wi = w[li];
         double acc = 0.0;
+#pragma unroll 4
         for (int lj = r1 + spart; lj < m; lj += T1_PARTS) {
           double* t = T + li + m * lj;
           const double tv = *t - vi * w[lj] - wi * v[lj];

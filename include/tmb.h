@@ -64,6 +64,14 @@ int tmb_ctx_destroy(tmb_ctx* ctx);
 int tmb_ctx_set_stream(tmb_ctx* ctx, void* cuda_stream);
 const char* tmb_last_error(const tmb_ctx* ctx);
 int64_t tmb_launch_count(const tmb_ctx* ctx); /* kernels launched so far */
+/* Workspace pool (caller owns every input/output buffer; the
+ * library owns one per-context pool of retained device chunks). Reports the
+ * reserved bytes and the high-water mark of bytes in use so far; reserve()
+ * replaces a smaller pool by one chunk of `bytes` (call between solves, e.g.
+ * with the peak of a first solve, so no later call allocates). No reference
+ * counterpart: the reference's numpy arrays are allocated per call. */
+int tmb_workspace_size(const tmb_ctx* ctx, int64_t* reserved_bytes, int64_t* peak_bytes);
+int tmb_workspace_reserve(tmb_ctx* ctx, int64_t bytes);
 /* Launch timing by kernel family (CUDA events on the context stream), used by
  * bench.py for the roofline: tags 0 DMMA GEMM (TTM/Gram), 1 tridiagonalisation,
  * 2 bisection+twisted vectors, 3 colour, 4 DMMA GEMMs inside the eigen-solver, 5 Ozaki int8

@@ -51,6 +51,8 @@ SIGNATURES = {
     "tmb_ctx_set_stream": ([_vp, _vp], _int),
     "tmb_last_error": ([_vp], C.c_char_p),
     "tmb_launch_count": ([_vp], _i64),
+    "tmb_workspace_size": ([_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
+    "tmb_workspace_reserve": ([_vp, C.c_int64], C.c_int),
     "tmb_timing": ([_vp, _int], _int),
     "tmb_timing_read": ([_vp, _int, _pi64, C.POINTER(_dbl), C.POINTER(_dbl)], _int),
     "tmb_color_u8": ([_vp, _vp, _i64, _i64, _i64, _int, _vp], _int),

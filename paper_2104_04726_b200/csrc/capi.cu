@@ -102,6 +102,21 @@ const char* tmb_last_error(const tmb_ctx* ctx) { return ctx ? ctx->c.err.c_str()
 
 int64_t tmb_launch_count(const tmb_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
 
+int tmb_workspace_size(const tmb_ctx* ctx, int64_t* reserved_bytes, int64_t* peak_bytes) {
+  if (!ctx) return TMB_EINVAL;
+  if (reserved_bytes) *reserved_bytes = (int64_t)ctx->c.arena.capacity();
+  if (peak_bytes) *peak_bytes = (int64_t)ctx->c.arena.peak();
+  return TMB_OK;
+}
+
+int tmb_workspace_reserve(tmb_ctx* ctx, int64_t bytes) {
+  if (bytes < 0) return TMB_EINVAL;
+  return guard(ctx, [&](tmb::Ctx& c) {
+    TMB_CUDA(cudaStreamSynchronize(c.stream));
+    c.arena.reserve((size_t)bytes);
+  });
+}
+
 int tmb_timing(tmb_ctx* ctx, int enable) {
   return guard(ctx, [&](tmb::Ctx& c) { tmb::timing_enable(c, enable != 0); });
 }

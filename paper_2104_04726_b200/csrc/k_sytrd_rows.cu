@@ -482,14 +482,20 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
       const int i = tid + NT * u;
       nr[u] = i == k + 2 ? 1.0 : (i >= k + 3 && i < N ? xa[u] * scale : 0.0);
     }
-    if (b == 0) {
-      if (tid == 0) { a.e[c1] = beta; a.tau[c1] = tau_n; }
+    // reflector k+1 to global: every block stores its own contiguous slice of
+    // rows (one block storing the whole column arrived ~190 cycles late at the
+    // next grid barrier, which every block then waited for)
+    if (b == 0 && tid == 0) { a.e[c1] = beta; a.tau[c1] = tau_n; }
+    {
+      const int S = (N + NB - 1) / NB, r0s = b * S;
       double* h = a.hv + n * c1;
 #pragma unroll
       for (int u = 0; u < RPT; ++u) {
         const int i = tid + NT * u;
-        if (i < N) h[i] = nr[u];
-        if (i == c1) a.d[c1] = xa[u];
+        if ((unsigned)(i - r0s) < (unsigned)S && i < N) {
+          h[i] = nr[u];
+          if (i == c1) a.d[c1] = xa[u];
+        }
       }
     }
     SM_T(5);
@@ -545,10 +551,16 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
     __syncthreads();
     SM_T(7);
     if (tid >= q0 && tid < nown) {
-      double s = 0.0;
+      // the NW warp partials of column tid: all loads first, then a pairwise
+      // tree (depth log2 NW instead of an NW-long dependent add chain)
+      double t[NW];
 #pragma unroll
-      for (int w = 0; w < NW; ++w) s += part[w * qmax + tid];
-      pbn[jb + (int64_t)NB * tid] = tau_n * s;
+      for (int w = 0; w < NW; ++w) t[w] = part[w * qmax + tid];
+#pragma unroll
+      for (int h = NW / 2; h > 0; h >>= 1)
+#pragma unroll
+        for (int w = 0; w < h; ++w) t[w] += t[w + h];
+      pbn[jb + (int64_t)NB * tid] = tau_n * t[0];
     }
 #pragma unroll
     for (int u = 0; u < RPT; ++u) {

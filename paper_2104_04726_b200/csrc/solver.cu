@@ -19,11 +19,17 @@ size_t Arena::capacity() const {
 
 void* Arena::alloc(size_t bytes) {
   bytes = std::max<size_t>(256, (bytes + 255) & ~size_t(255));
+  const auto track = [&] {
+    size_t in_use = 0;
+    for (size_t j = 0; j <= cur_ && j < chunks_.size(); ++j) in_use += chunks_[j].used;
+    peak_ = std::max(peak_, in_use);
+  };
   while (cur_ < chunks_.size()) {
     Chunk& c = chunks_[cur_];
     if (c.cap - c.used >= bytes) {
       void* p = c.p + c.used;
       c.used += bytes;
+      track();
       return p;
     }
     if (cur_ + 1 < chunks_.size() && chunks_[cur_ + 1].cap >= bytes) { ++cur_; continue; }
@@ -40,7 +46,17 @@ void* Arena::alloc(size_t bytes) {
   const size_t pos = chunks_.empty() ? 0 : cur_ + 1;
   chunks_.insert(chunks_.begin() + pos, Chunk{p, cap, bytes});
   cur_ = pos;
+  track();
   return p;
+}
+
+// Called between API calls only (no live allocations; the caller synchronised
+// the stream): replaces a smaller pool by one retained chunk of `bytes`.
+void Arena::reserve(size_t bytes) {
+  if (bytes == 0 || capacity() >= bytes) return;
+  free_all();
+  alloc(bytes);
+  release(0);
 }
 
 size_t Arena::mark() const {

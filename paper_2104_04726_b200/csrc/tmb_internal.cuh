@@ -43,11 +43,14 @@ class Arena {
   void release(size_t mark);
   void free_all();
   size_t capacity() const;
+  size_t peak() const { return peak_; }  // high-water mark of bytes in use
+  void reserve(size_t bytes);            // one retained chunk of at least `bytes`
 
  private:
   struct Chunk { char* p; size_t cap; size_t used; };
   std::vector<Chunk> chunks_;
   size_t cur_ = 0;
+  size_t peak_ = 0;
 };
 
 // Per-family launch timing (CUDA events on the context stream), enabled by the

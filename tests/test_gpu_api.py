@@ -408,3 +408,28 @@ def test_launch_counter_advances():
     n0 = L.launch_count()
     tb.gram(np.ones((3, 4)))
     assert L.launch_count() > n0
+
+
+def test_workspace_pool_query_and_reserve():
+    """the library's own per-context pool; after one solve the
+    high-water mark is known, reserving it up front means later solves of the
+    same shape allocate nothing new (the reserved capacity does not grow)."""
+    import ctypes as C
+
+    h = L.ctx()
+    rng = np.random.default_rng(31)
+    x = tb.DenseTensor(rng.standard_normal((40, 50, 3, 6)))
+    cfg = tb.SolveConfig(ranks=(8, 9, 3, 3), max_sweeps=3, fit_tol=1e-300, pp_enter_tol=0.0)
+    tb.tucker_als(x, cfg)
+    res, peak = C.c_int64(), C.c_int64()
+    L.check(L.LIB.tmb_workspace_size(h, C.byref(res), C.byref(peak)), h)
+    assert 0 < peak.value <= res.value
+    L.check(L.LIB.tmb_workspace_reserve(h, res.value + (64 << 20)), h)
+    res2 = C.c_int64()
+    L.check(L.LIB.tmb_workspace_size(h, C.byref(res2), C.byref(peak)), h)
+    assert res2.value >= res.value + (64 << 20)
+    tb.tucker_als(x, cfg)
+    res3 = C.c_int64()
+    L.check(L.LIB.tmb_workspace_size(h, C.byref(res3), C.byref(peak)), h)
+    assert res3.value == res2.value
+    assert L.LIB.tmb_workspace_reserve(h, -1) != 0

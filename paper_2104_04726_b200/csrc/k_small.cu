@@ -77,6 +77,63 @@ __global__ void k_small_ttm(const T* __restrict__ x, int64_t L, int K, int64_t R
   }
 }
 
+// ---- two consecutive small-mode TTMs in one pass (modes m, m+1 both small):
+// y[l + L(i1 + r1 (i2 + r2 rr))] = sum_k2 M2(i2,k2) sum_k1 M1(i1,k1) x[l + L(k1 + K1 (k2 + K2 rr))]
+// One thread per (l, rr) fiber: the K1 x K2 inputs are read once, the inner
+// sums t(i1, k2) stay in registers, the r1 x r2 outputs are written once. Each
+// sum runs in the same order with the same fma as k_small_ttm, so the result
+// is bitwise that of the two separate passes (which read and write the
+// intermediate through HBM).
+constexpr int ST2_THREADS = 128, ST2_R1 = 8, ST2_T = 64;  // r1 <= 8, K2 * r1 <= 64
+template <typename T>
+__global__ void __launch_bounds__(ST2_THREADS) k_small_ttm2(const T* __restrict__ x, int64_t L, int K1, int K2,
+                                                            int64_t Rr, const double* __restrict__ m1, int r1,
+                                                            int64_t s1r, int64_t s1k, const double* __restrict__ m2,
+                                                            int r2, int64_t s2r, int64_t s2k, double* __restrict__ y) {
+  extern __shared__ double sm2[];
+  double* A1 = sm2;                  // [k1][i1]
+  double* A2 = A1 + K1 * r1;         // [k2][i2]
+  double* tb = A2 + K2 * r2;         // per-thread t(i1, k2) at tb[(k2 * r1 + i1) * ST2_THREADS + tid]
+  const int tid = threadIdx.x;
+  for (int e = tid; e < K1 * r1; e += blockDim.x) A1[e] = m1[(e % r1) * s1r + (e / r1) * s1k];
+  for (int e = tid; e < K2 * r2; e += blockDim.x) A2[e] = m2[(e % r2) * s2r + (e / r2) * s2k];
+  __syncthreads();
+  const int64_t total = L * Rr;
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + tid; f < total; f += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = f % L, rr = f / L;
+    const T* xp = x + l + L * (int64_t)K1 * K2 * rr;
+    for (int k2 = 0; k2 < K2; ++k2) {  // first TTM: t(i1, k2) = sum_k1 M1(i1,k1) x(k1, k2)
+      double acc[ST2_R1];
+#pragma unroll
+      for (int i = 0; i < ST2_R1; ++i) acc[i] = 0.0;
+      for (int k1 = 0; k1 < K1; ++k1) {
+        const double xv = ld(xp, L * (k1 + (int64_t)K1 * k2));
+#pragma unroll
+        for (int i = 0; i < ST2_R1; ++i)
+          if (i < r1) acc[i] = fma(A1[k1 * r1 + i], xv, acc[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < ST2_R1; ++i)
+        if (i < r1) tb[(k2 * r1 + i) * ST2_THREADS + tid] = acc[i];
+    }
+    double* yp = y + l + L * (int64_t)r1 * r2 * rr;
+    for (int i2 = 0; i2 < r2; ++i2) {  // second TTM: y(i1, i2) = sum_k2 M2(i2,k2) t(i1, k2)
+      double acc[ST2_R1];
+#pragma unroll
+      for (int i = 0; i < ST2_R1; ++i) acc[i] = 0.0;
+      for (int k2 = 0; k2 < K2; ++k2) {
+        const double a = A2[k2 * r2 + i2];
+#pragma unroll
+        for (int i = 0; i < ST2_R1; ++i)
+          if (i < r1) acc[i] = fma(a, tb[(k2 * r1 + i) * ST2_THREADS + tid], acc[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < ST2_R1; ++i)
+        if (i < r1) yp[L * (i + (int64_t)r1 * i2)] = acc[i];
+    }
+  }
+}
+
 // ---- small-mode Gram, pass 1: per-block partial upper-triangle sums.
 constexpr int SG_THREADS = 256, SG_MAXPP = 9;  // K <= 64 -> 2080 pairs <= 9*256
 template <typename T>
@@ -341,6 +398,24 @@ void small_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t Rr
   else
     k_small_ttm<double><<<blocks, 256, smem, c.stream>>>((const double*)x, L, (int)K, Rr, m, (int)r, sMr, sMk, y);
   LAUNCHED("k_small_ttm");
+}
+
+bool small_ttm2(Ctx& c, const void* x, DType tx, int64_t L, int64_t K1, int64_t K2, int64_t Rr, const double* m1,
+                int64_t r1, int64_t s1r, int64_t s1k, const double* m2, int64_t r2, int64_t s2r, int64_t s2k,
+                double* y) {
+  if (r1 > ST2_R1 || K2 * r1 > ST2_T || K1 > 64 || K2 > 64 || r2 > 64) return false;
+  const int64_t total = L * Rr;
+  if (total == 0) return true;
+  const size_t smem = sizeof(double) * (K1 * r1 + K2 * r2 + (size_t)K2 * r1 * ST2_THREADS);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, ST2_THREADS), 32LL * c.num_sms));
+  if (tx == F32)
+    k_small_ttm2<float><<<blocks, ST2_THREADS, smem, c.stream>>>((const float*)x, L, (int)K1, (int)K2, Rr, m1,
+                                                                  (int)r1, s1r, s1k, m2, (int)r2, s2r, s2k, y);
+  else
+    k_small_ttm2<double><<<blocks, ST2_THREADS, smem, c.stream>>>((const double*)x, L, (int)K1, (int)K2, Rr, m1,
+                                                                   (int)r1, s1r, s1k, m2, (int)r2, s2r, s2k, y);
+  LAUNCHED("k_small_ttm2");
+  return true;
 }
 
 void small_gram(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t Rr, double* g) {

@@ -482,20 +482,14 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
       const int i = tid + NT * u;
       nr[u] = i == k + 2 ? 1.0 : (i >= k + 3 && i < N ? xa[u] * scale : 0.0);
     }
-    // reflector k+1 to global: every block stores its own contiguous slice of
-    // rows (one block storing the whole column arrived ~190 cycles late at the
-    // next grid barrier, which every block then waited for)
-    if (b == 0 && tid == 0) { a.e[c1] = beta; a.tau[c1] = tau_n; }
-    {
-      const int S = (N + NB - 1) / NB, r0s = b * S;
+    if (b == 0) {
+      if (tid == 0) { a.e[c1] = beta; a.tau[c1] = tau_n; }
       double* h = a.hv + n * c1;
 #pragma unroll
       for (int u = 0; u < RPT; ++u) {
         const int i = tid + NT * u;
-        if ((unsigned)(i - r0s) < (unsigned)S && i < N) {
-          h[i] = nr[u];
-          if (i == c1) a.d[c1] = xa[u];
-        }
+        if (i < N) h[i] = nr[u];
+        if (i == c1) a.d[c1] = xa[u];
       }
     }
     SM_T(5);
@@ -613,6 +607,7 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
   }();
   const int nb = nb_env > 0 ? std::min(nb_env, bps * c.num_sms) : bps * c.num_sms;
   const int rpt = (int)ceil_div(n, nt);
+  static const bool rpt4_env = std::getenv("TMB_SMEM_RPT4") != nullptr;  // A/B: 4 rows/thread for n <= 1536
   using KFn = void (*)(RowArgs, int, long long*);
   KFn kern = nullptr;
   int slot = 0;
@@ -621,6 +616,7 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
 #define SMEM_K(R, T) (prof_on ? k_sytrd_smem<R, T, true> : k_sytrd_smem<R, T, false>)
   if (nt == 512) {
     if (rpt <= 2) { kern = SMEM_K(2, 512); slot = 0; }
+    else if (rpt <= 3 && !rpt4_env) { kern = SMEM_K(3, 512); slot = 4; }  // n <= 1536 (C2 mode 0)
     else if (rpt <= 4) { kern = SMEM_K(4, 512); slot = 1; }
   } else {
     if (rpt <= 4) { kern = SMEM_K(4, 256); slot = 2; }
@@ -631,7 +627,7 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
   const int nw = nt / 32;
   const size_t smem = sizeof(double) * (((size_t)qmax * n + 1) / 2 * 2 + (size_t)nw * qmax + 2 * nw + 2 * qmax + 1);
   if (smem > 227 * 1024) return false;
-  static int64_t checked[4] = {-1, -1, -1, -1};
+  static int64_t checked[5] = {-1, -1, -1, -1, -1};
   if (checked[slot] != n) {
     TMB_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)std::max<size_t>(smem, 48 * 1024)));

@@ -4,6 +4,8 @@
 // control-flow scalars (fit, factor change) read back once per sweep.
 #include "solver.h"
 
+#include <cstdlib>
+
 namespace tmb {
 
 // ------------------------------------------------------------------ Arena
@@ -287,6 +289,7 @@ void hooi_sweep_dev(Ctx& c, const void* x, DType tx, const Dims& dims, const Dim
     c.arena.release(mk);
     return;
   }
+  static const bool fuse_off = std::getenv("TMB_NO_TTM2") != nullptr;  // A/B: separate small-mode passes
   const void* P = x;  // prefix product with updated factors 0..n-1
   DType pt = tx;
   Dims pd = dims;
@@ -298,6 +301,18 @@ void hooi_sweep_dev(Ctx& c, const void* x, DType tx, const Dims& dims, const Dim
     for (int m = n + 1; m < N; ++m) {
       Dims nd = yd;
       nd[m] = ranks[m];
+      // two trailing small modes (colour, view-exposure): one fused pass
+      if (m + 1 < N && !fuse_off && yd[m] <= 64 && ranks[m] <= 64 && yd[m + 1] <= 64 && ranks[m + 1] <= 64) {
+        Dims nd2 = nd;
+        nd2[m + 1] = ranks[m + 1];
+        double* dst = alloc<double>(c, (size_t)prod(nd2, 0, N));
+        if (small_ttm2(c, Y, yt, prod(yd, 0, m), yd[m], yd[m + 1], prod(yd, m + 2, N), cur[m], ranks[m], dims[m], 1,
+                       cur[m + 1], ranks[m + 1], dims[m + 1], 1, dst)) {
+          Y = dst; yt = F64; yd = nd2;
+          ++m;
+          continue;
+        }
+      }
       double* dst = alloc<double>(c, (size_t)prod(nd, 0, N));
       ttm_dev(c, Y, yt, yd, m, cur[m], ranks[m], dims[m], 1, dst);
       Y = dst; yt = F64; yd = nd;

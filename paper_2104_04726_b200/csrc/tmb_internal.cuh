@@ -117,6 +117,11 @@ void mirror_upper(Ctx& c, double* g, int64_t n, int batch, int64_t sb);
 // ---------------------------------------------------------------- small kernels (k_small.cu)
 void small_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t Rr,
                const double* m, int64_t r, int64_t sMr, int64_t sMk, double* y);
+// two consecutive small-mode TTMs (modes m, m+1) in one pass, bitwise equal to
+// two small_ttm calls; false (nothing launched) outside its size limits
+bool small_ttm2(Ctx& c, const void* x, DType tx, int64_t L, int64_t K1, int64_t K2, int64_t Rr, const double* m1,
+                int64_t r1, int64_t s1r, int64_t s1k, const double* m2, int64_t r2, int64_t s2r, int64_t s2k,
+                double* y);
 void small_gram(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t Rr, double* g);
 double sumsq(Ctx& c, const void* x, DType tx, int64_t n);           // sync D2H
 void sumsq_async(Ctx& c, const void* x, DType tx, int64_t n, double* out_dev);

@@ -433,7 +433,30 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) k_sytrd(const TrdArgs a) {
 template <int P>
 __device__ __forceinline__ void sturm_counts(const double* __restrict__ d, const double* __restrict__ e,
                                              int64_t n, const double (&x)[P], double pivmin, int (&cnt)[P]) {
+  // Fast path: the recurrence without the pivmin guard, whose test and select
+  // would sit on the loop-carried chain; the guard only changes the sequence
+  // once some |q| <= pivmin, which the off-chain flag records, and then the
+  // chain is recomputed exactly as dstebz does (guarded), so the counts are
+  // those of the guarded recurrence in every case.
   double q[P];
+  bool hit = false;
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    q[p] = d[0] - x[p];
+    hit |= fabs(q[p]) <= pivmin;
+    cnt[p] = q[p] < 0.0;
+  }
+  for (int64_t i = 1; i < n; ++i) {
+    const double ei = e[i - 1], di = d[i];
+    const double e2 = ei * ei;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      q[p] = (di - x[p]) - e2 * frcp(q[p]);
+      hit |= fabs(q[p]) <= pivmin;
+      cnt[p] += q[p] < 0.0;
+    }
+  }
+  if (!hit) return;
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     q[p] = d[0] - x[p];
@@ -716,43 +739,59 @@ __global__ void __launch_bounds__(64) k_twisted_sm(const double* __restrict__ d,
   for (int o = 16; o > 0; o >>= 1) emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
   const double pivmin = DBL_MIN * fmax(1.0, emax2);
   constexpr int U = 8;
+  // Each chain first runs without the pivmin guard (its test and select would
+  // sit on the loop-carried path); the off-chain flag records whether it would
+  // ever have fired, and only then is the chain recomputed guarded, so the
+  // stored pivots always equal the guarded recurrence's (as in sturm_counts).
   if (wib == 0 && lane == 0) {  // D+ (stationary qd, top-down)
-    double q = d[0] - lam;
-    if (fabs(q) <= pivmin) q = -pivmin;
-    dpj[0] = q;
-    for (int64_t i0 = 1; i0 < n; i0 += U) {
-      double dv[U], ev[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        dv[u] = i0 + u < n ? d[i0 + u] : 0.0;
-        ev[u] = i0 + u < n ? e[i0 + u - 1] : 0.0;
-      }
+    for (int guarded = 0; guarded < 2; ++guarded) {  // unrolled: two specialised chains
+      double q = d[0] - lam;
+      bool hit = fabs(q) <= pivmin;
+      if (guarded && hit) q = -pivmin;
+      dpj[0] = q;
+      for (int64_t i0 = 1; i0 < n; i0 += U) {
+        double dv[U], ev[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (i0 + u >= n) break;
-        q = (dv[u] - lam) - ev[u] * ev[u] * frcp(q);
-        if (fabs(q) <= pivmin) q = -pivmin;
-        dpj[i0 + u] = q;
+        for (int u = 0; u < U; ++u) {
+          dv[u] = i0 + u < n ? d[i0 + u] : 0.0;
+          ev[u] = i0 + u < n ? e[i0 + u - 1] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (i0 + u >= n) break;
+          q = (dv[u] - lam) - ev[u] * ev[u] * frcp(q);
+          hit |= fabs(q) <= pivmin;
+          if (guarded && fabs(q) <= pivmin) q = -pivmin;
+          dpj[i0 + u] = q;
+        }
       }
+      if (!hit) break;
     }
   } else if (wib == 1 && lane == 0) {  // D- (progressive qd, bottom-up)
-    double m = d[n - 1] - lam;
-    if (fabs(m) <= pivmin) m = -pivmin;
-    dmj[n - 1] = m;
-    for (int64_t i0 = n - 2; i0 >= 0; i0 -= U) {
-      double dv[U], ev[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        dv[u] = i0 - u >= 0 ? d[i0 - u] : 0.0;
-        ev[u] = i0 - u >= 0 ? e[i0 - u] : 0.0;
-      }
+    for (int guarded = 0; guarded < 2; ++guarded) {  // unrolled: two specialised chains
+      double m = d[n - 1] - lam;
+      bool hit = fabs(m) <= pivmin;
+      if (guarded && hit) m = -pivmin;
+      dmj[n - 1] = m;
+      for (int64_t i0 = n - 2; i0 >= 0; i0 -= U) {
+        double dv[U], ev[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (i0 - u < 0) break;
-        const double t = (dv[u] - lam) - ev[u] * ev[u] * frcp(m);
-        m = fabs(t) <= pivmin ? -pivmin : t;
-        dmj[i0 - u] = m;
+        for (int u = 0; u < U; ++u) {
+          dv[u] = i0 - u >= 0 ? d[i0 - u] : 0.0;
+          ev[u] = i0 - u >= 0 ? e[i0 - u] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (i0 - u < 0) break;
+          const double t = (dv[u] - lam) - ev[u] * ev[u] * frcp(m);
+          hit |= fabs(t) <= pivmin;
+          m = (guarded && fabs(t) <= pivmin) ? -pivmin : t;
+          dmj[i0 - u] = m;
+        }
       }
+      if (!hit) break;
     }
   }
   __syncthreads();

@@ -248,6 +248,27 @@ def test_hooi_matches_oracle_sweep():
     assert np.abs(m1.core.array - core1).max() < 1e-10
 
 
+@pytest.mark.parametrize("dims,ranks", [
+    ((20, 24, 3, 18), (5, 6, 3, 9)),    # C5-like trailing modes: fused pass with > 48 KB of inner sums
+    ((20, 24, 3, 10), (5, 6, 3, 5)),    # C2-like: fused pass
+    ((12, 14, 12, 10), (4, 5, 9, 5)),   # r1 = 9 > 8: separate small-mode passes
+])
+def test_hooi_small_mode_paths_match_oracle(dims, ranks):
+    """The sweep's trailing small-mode contractions (fused two-mode pass or two
+    separate passes) against the oracle's ascending ttmc."""
+    rng = np.random.default_rng(sum(dims))
+    x = rng.standard_normal(dims)
+    m0 = tb.t_hosvd(tb.DenseTensor(x), ranks)
+    core_o, fac_o = oracle.t_hosvd(x, ranks)
+    m1 = tb.hooi_sweep(tb.DenseTensor(x), m0)
+    core1, fac1 = oracle.hooi_sweep(x, fac_o)
+    from conftest import principal_angle
+
+    for a, b in zip(m1.factors, fac1):
+        assert principal_angle(a, b) < 1e-8
+    assert abs(np.linalg.norm(m1.core.array) - np.linalg.norm(core1)) < 1e-10 * np.linalg.norm(core1)
+
+
 def test_fit_and_reconstruct_contracts():  # tests/test_tucker.py:169-254
     rng = np.random.default_rng(11)
     t = tb.DenseTensor(rng.standard_normal((6, 5, 4)))

@@ -298,6 +298,24 @@ def run_ours(args) -> None:
                  "achieved": col_gbs, "peak": hbm_peak, "frac": col_gbs / hbm_peak if col_gbs else None,
                  "bytes_per_launch": col["work"] / max(col["launches"], 1)}
 
+    # the contraction kernels on the FP64 tensor pipe (TTM full passes on DMMA, Grams) and the
+    # Ozaki tcgen05 TTM, same live timing, algorithmic flops (SURVEY 8(d) counting rules)
+    roof_gemm = {}
+    for nm in ("gemm_dmma", "ttm_ozaki_i8"):
+        f = fam[nm]
+        if f["ms"] > 0:
+            tf = f["work"] / (f["ms"] / 1e3) / 1e12
+            roof_gemm[nm] = {"achieved": tf, "unit": "TFLOP/s (fp64-equivalent)", "peak": FP64_PEAK_TFLOPS,
+                             "frac": tf / FP64_PEAK_TFLOPS, "ms_per_step": f["ms"] / args.steps}
+    # the tridiagonalisation is latency-bound: per-column time against the measured
+    # 148-block grid-barrier floor (2.5k cycles at 1965 MHz, scripts/research/barrier_bench.cu)
+    sy = fam["sytrd"]
+    cols = sum(n - 1 for n in cfg.dims[:2]) * (cfg.sweeps + 1)
+    per_col_us = 1e3 * sy["ms"] / args.steps / cols
+    roof["latency"] = {"per_column_us": per_col_us, "grid_barrier_floor_us": 2500 / 1965.0,
+                       "columns_per_step": cols,
+                       "note": "one grid barrier + two block reductions + one L2 gather per column"}
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -314,6 +332,7 @@ def run_ours(args) -> None:
         "gpu_launches": int(launches),
         "roofline": roof,
         "roofline_elementwise": roof_elem,
+        "roofline_contractions": roof_gemm,
         "kernel_families": {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps}
                             for k, v in fam.items()},
         "clocks": clk,

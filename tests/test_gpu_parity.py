@@ -43,6 +43,41 @@ def test_golden_parity(golden, name):
     res.model.validate()
 
 
+def test_c2_full_size_matches_reference(golden):
+    """The bench workload itself (BASELINE config 2 at full size, seed 0) against
+    the reference run in the build container (scripts/make_golden_c2_full.py):
+    trace fits, relative error, quantiser step, every quantised level (bit-exact
+    except rounding ties), the factor subspaces through a fixed
+    rotation-invariant sketch W^T U U^T W, and the leading sign-fixed columns."""
+    import hashlib
+
+    z = golden("c2_full")
+    cfg = CONFIGS["c2"]
+    images = make_stack(cfg, seed=0)
+    t = tb.coding_tensor(images, cfg.space).cpu().numpy()
+    assert hashlib.sha256(t.tobytes()).hexdigest() == str(z["tensor_f32_sha"])  # same stack, bit for bit
+    res = tb.encode_stack(images, cfg.space, cfg.ranks, cfg.sweeps, cfg.qp)
+    fits = np.array([r.fit for r in res.trace.records])
+    m = min(len(fits), len(z["trace_fit"]))
+    assert m == len(z["trace_fit"])
+    assert np.abs(fits[:m] - z["trace_fit"][:m]).max() < 1e-9
+    assert abs(res.rel_err - float(z["rel_err"])) < 1e-8          # bar 1e-4
+    assert float(res.step) == pytest.approx(float(z["step"]), rel=1e-12)
+    for n in range(4):
+        u = res.model.factors[n]
+        w = np.random.default_rng(1000 + u.shape[0]).standard_normal((u.shape[0], 16)) / np.sqrt(u.shape[0])
+        p = w.T @ u
+        assert np.abs(p @ p.T - z[f"sketch{n}"]).max() < 1e-6    # subspace (bar 1e-3 rad)
+        h = z[f"head{n}"]
+        assert np.abs(u[:, : h.shape[1]] - h).max() < 1e-6        # leading eigenvectors, same sign rule
+    lv = res.levels.astype(np.int64)
+    ref = z["levels"].astype(np.int64)
+    diff = lv != ref
+    # bit-exact except rounding ties: at most 1 LSB, on a vanishing fraction of the 1.94 M levels
+    assert (np.abs(lv - ref).max() if diff.any() else 0) <= 1
+    assert diff.sum() <= 1e-5 * lv.size, int(diff.sum())
+
+
 def test_c2_full_size_properties():
     """BASELINE config 2 at full size: orthonormality, monotone fit, the
     ||t||^2 - ||core||^2 identity vs the explicit reconstruction, quantiser

@@ -14,6 +14,7 @@
 // grid kernel stopped: v_{K0} in hv column K0, tau_{K0} in tau, the trailing
 // block (rows/columns >= K0+1) of A updated through step K0-1.
 // Deterministic: fixed reduction trees.
+#include <cstdio>
 #include <cstdlib>
 
 #include "tmb_internal.cuh"
@@ -44,7 +45,9 @@ constexpr int T1_PARTS = T1_THREADS / 256;      // symv: 256 rows x 4 column str
 
 __global__ void __launch_bounds__(T1_THREADS, 1) k_sytrd_tail1(double* __restrict__ A, int64_t n, int64_t K0,
                                                               double* __restrict__ d, double* __restrict__ e,
-                                                              double* __restrict__ tau, double* __restrict__ hv) {
+                                                              double* __restrict__ tau, double* __restrict__ hv,
+                                                              long long* __restrict__ prof) {
+  long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;  // TMB_TRD_PROFILE: per-phase cycles summed over the columns
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t base = K0 + 1;
   const int m = (int)(n - base);
@@ -72,6 +75,7 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_sytrd_tail1(double* __restric
   __syncthreads();
 
   for (int64_t k = K0; k + 2 < n; ++k) {
+    if (prof && threadIdx.x == 0) t0 = clock64();
     const int r0 = (int)(k + 1 - base);  // local index of column k+1
     if (warp == 0) {
       // lane owns live rows li = r0 + lane + 32 q; the scalar chain stays in registers
@@ -138,6 +142,7 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_sytrd_tail1(double* __restric
       }
     }
     __syncthreads();
+    if (prof && threadIdx.x == 0) t1 = clock64();
     if (k + 3 == n) break;
     // reflector k+1 into hv (full column, zero above row k+2)
     {
@@ -163,8 +168,13 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_sytrd_tail1(double* __restric
     }
     tau_k = sc[1];
     __syncthreads();
+    if (prof && threadIdx.x == 0) t2 = clock64();
     for (int li = r0 + 1 + tid; li < m; li += T1_THREADS) v[li] = x[li];
     __syncthreads();
+    if (prof && threadIdx.x == 0) {
+      t3 = clock64();
+      prof[0] += t1 - t0; prof[1] += t2 - t1; prof[2] += t3 - t2; prof[3] += 1;
+    }
   }
 }
 
@@ -190,9 +200,23 @@ void sytrd_tail1(Ctx& c, double* A, int64_t n, int64_t K0, double* d, double* e,
                                   (int)(sizeof(double) * (T1_MAX * T1_MAX + (3 + T1_PARTS) * T1_MAX + 2))));
     attr = true;
   }
-  k_sytrd_tail1<<<1, T1_THREADS, smem, c.stream>>>(A, n, K0, d, e, tau, hv);
+  static const bool prof_on = std::getenv("TMB_TRD_PROFILE") != nullptr;
+  long long* prof = nullptr;
+  if (prof_on) {
+    prof = alloc<long long>(c, 4);
+    TMB_CUDA(cudaMemsetAsync(prof, 0, 4 * sizeof(long long), c.stream));
+  }
+  k_sytrd_tail1<<<1, T1_THREADS, smem, c.stream>>>(A, n, K0, d, e, tau, hv, prof);
   c.launches++;
   check_launch("k_sytrd_tail1");
+  if (prof) {
+    long long h[4];
+    TMB_CUDA(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    TMB_CUDA(cudaStreamSynchronize(c.stream));
+    if (h[3])
+      std::fprintf(stderr, "sytrd_tail1 n=%lld m=%lld cycles/column: scalars+bar %lld | hv+pass+bar %lld | copy+bar %lld\n",
+                   (long long)n, (long long)m, h[0] / h[3], h[1] / h[3], h[2] / h[3]);
+  }
 }
 
 }  // namespace tmb

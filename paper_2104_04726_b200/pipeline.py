@@ -93,11 +93,21 @@ def encode_stack(images_u8: np.ndarray, space: str, ranks: Sequence[int], sweeps
     cfg = SolveConfig(ranks=tuple(ranks), max_sweeps=sweeps, fit_tol=fit_tol, pp_enter_tol=pp_enter_tol)
     bufs, tr, step, rel = encode_stack_device(imgs, space, ranks, cfg, qp, rel_err=rel_err)
     ranks = tuple(int(r) for r in ranks)
-    levels = np.reshape(bufs["levels"][: int(np.prod(ranks))].cpu().numpy(), ranks, order="F")
+    # D2H into pinned host tensors (torch's caching host allocator), one sync for all;
+    # the returned arrays keep their pinned blocks alive
+    ncore = int(np.prod(ranks))
+    outs = [bufs["levels"][:ncore]]
+    if return_model:
+        outs += [bufs["core"][:ncore]] + [f[: dims[n] * ranks[n]] for n, f in enumerate(bufs["factors"])]
+    host = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
+    for h_, o in zip(host, outs):
+        h_.copy_(o, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    levels = np.reshape(host[0].numpy(), ranks, order="F")
     model = None
     if return_model:
-        core = DenseTensor(L.host_f(bufs["core"], ranks))
-        facs = [L.host_f(f, (dims[n], ranks[n])) for n, f in enumerate(bufs["factors"])]
+        core = DenseTensor(np.reshape(host[1].numpy(), ranks, order="F"))
+        facs = [np.reshape(host[2 + n].numpy(), (dims[n], ranks[n]), order="F") for n in range(len(dims))]
         model = TuckerModel(core, facs, dims)
     return StackResult(model, _trace_from_c(tr), levels, step, rel, bufs)
 

@@ -41,7 +41,11 @@ __device__ __forceinline__ double frcp1(double b) {
 
 constexpr int T1_MAX = 160;                     // trailing block capacity (227 KB of shared memory)
 constexpr int T1_RPL = (T1_MAX + 31) / 32;      // live rows per lane of warp 0
-constexpr int T1_PARTS = T1_THREADS / 256;      // symv: 256 rows x 4 column strides
+#ifndef TMB_T1_PARTS
+#define TMB_T1_PARTS 4
+#endif
+constexpr int T1_PARTS = TMB_T1_PARTS;          // symv: T1_THREADS / T1_PARTS rows x T1_PARTS column strides
+constexpr int T1_ROWS = T1_THREADS / T1_PARTS;
 
 __global__ void __launch_bounds__(T1_THREADS, 1) k_sytrd_tail1(double* __restrict__ A, int64_t n, int64_t K0,
                                                               double* __restrict__ d, double* __restrict__ e,
@@ -63,14 +67,11 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_sytrd_tail1(double* __restric
   for (int li = tid; li < m; li += T1_THREADS) v[li] = hv[(base + li) + n * K0];
   double tau_k = tau[K0];
   __syncthreads();
-  const int srow = tid & 255, spart = tid >> 8;
-  {  // p_{K0} partials (no update pending)
-    const int li = srow;
-    if (li < m) {
-      double acc = 0.0;
-      for (int lj = spart; lj < m; lj += T1_PARTS) acc = fma(T[li + m * lj], v[lj], acc);
-      pp[spart * m + li] = acc;
-    }
+  const int srow = tid % T1_ROWS, spart = tid / T1_ROWS;
+  for (int li = srow; li < m; li += T1_ROWS) {  // p_{K0} partials (no update pending)
+    double acc = 0.0;
+    for (int lj = spart; lj < m; lj += T1_PARTS) acc = fma(T[li + m * lj], v[lj], acc);
+    pp[spart * m + li] = acc;
   }
   __syncthreads();
 
@@ -151,9 +152,9 @@ __global__ void __launch_bounds__(T1_THREADS, 1) k_sytrd_tail1(double* __restric
     }
     // fused pass over the block that stays live (rows/columns >= r0+1): rank-2
     // update of step k and, through the symmetry of T, the row sums of p_{k+1}
-    {
-      const int r1 = r0 + 1, li = r1 + srow;
-      if (li < m) {
+    for (int li = r0 + 1 + srow; li < m; li += T1_ROWS) {
+      const int r1 = r0 + 1;
+      {
         const double vi = v[li], wi = w[li];
         double acc = 0.0;
 #pragma unroll 4

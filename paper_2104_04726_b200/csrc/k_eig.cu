@@ -1462,11 +1462,13 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
     const char* s = std::getenv("TMB_SYTRD_TAIL");  // A/B switch: max trailing size, 0 = off
     return s ? std::atoll(s) : (int64_t)-1;
   }();
-  // Measured (scripts/ab_tail.sh): the cluster kernel wins for whole solves up
-  // to n ~ 400 (n=300: 1.63 vs 1.80 ms) but loses as a tail of larger solves
-  // (n=600: 4.2 vs 3.7 ms), so by default it only takes small matrices whole.
+  // Measured (scripts/bench_eig.py, TMB_SYTRD_TAIL=0 A/B): the cluster kernel
+  // wins for whole solves up to n ~ 250 (n=250: 0.76 vs 0.81 ms) and loses from
+  // n ~ 300 on to the shared-memory grid kernel + single-CTA tail (n=300: 1.00
+  // vs 0.95 ms, n=384: 1.45 vs 1.21 ms), and as a tail of larger solves, so by
+  // default it only takes small matrices whole.
   const int64_t cap = sytrd_tail_capacity(c);
-  int64_t K0 = (n - 1 <= std::min<int64_t>(cap, 400)) ? 0 : n;
+  int64_t K0 = (n - 1 <= std::min<int64_t>(cap, 280)) ? 0 : n;
   if (tail_env >= 0) {
     const int64_t tail_m = std::min(cap, tail_env);
     K0 = tail_m >= 2 ? std::max<int64_t>(0, n - 1 - tail_m) : n;

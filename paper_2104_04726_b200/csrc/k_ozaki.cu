@@ -386,6 +386,214 @@ __global__ void __launch_bounds__(OZ_NT, 1) k_oz_gemm(const __grid_constant__ CU
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// ---------------------------------------------------------------- N = 128 variant
+// Same products, tiles of 128 factor rows x 128 tensor rows. Eight 128-column
+// shift-group accumulators would need 1024 TMEM columns, so the 36 digit
+// products run in three K passes over two halves of TMEM:
+//   hi-1: s in 0..3, t = g - s for g in 4..7 (16 products; A planes 0-3, B planes 1-7)
+//   hi-2: s in 4..7, t = g - s for g in 4..7 (10 products; A planes 4-7, B planes 0-3)
+//   lo:   g in 0..3, s + t = g              (10 products; A planes 0-3, B planes 0-3)
+// Groups 4-7 (hi) accumulate in TMEM columns (g-4)*128; after hi-2 the four
+// epilogue warps fold them into sum_{g=7..4} acc_g 2^(-12-7g) and park that
+// partial in y, TMEM is handed back, lo reuses it for groups 0-3, and the
+// final epilogue continues the same fma chain (g = 3..0) from the parked
+// partial before the 2^(e_r+e_m) scaling -- bitwise the N = 64 kernel's sum.
+// Per 128x128x32 MMA the tensor core reads 8 KB of shared memory (4 KB per
+// operand) against 6 KB per 128x64x32 before: the operand port was the bound.
+// Warps: 0-3 epilogue (TMEM lane quarters), 4 TMA producer, 5 MMA issuer.
+constexpr int OZ2_BN = 128, OZ2_NT = 192, OZ2_ST = 2;
+constexpr uint32_t OZ2_PLANE = 128 * OZ_BK;              // 8 KB: one digit plane of a 128-row tile
+constexpr uint32_t OZ2_STAGE = 4 * OZ2_PLANE + 7 * OZ2_PLANE;  // 88 KB (A 4 planes + B up to 7)
+
+template <int PHASE>  // 0: groups 7..4 -> partial into y; 1: partial + groups 3..0, scaled
+__device__ __forceinline__ void oz2_epilogue(uint32_t tmem, int warp, int lane, int64_t m0, int64_t n0,
+                                             const int* __restrict__ eu, const int* __restrict__ ex, int64_t L,
+                                             int64_t R, int64_t N, double* __restrict__ y) {
+  const int64_t r = m0 + warp * 32 + lane;
+  const bool rok = r < N;
+  const int er = rok ? eu[r] : 0;
+  const int64_t MX = L * R;
+  int64_t ib = n0 % L, lb = n0 / L;
+  for (int c0 = 0; c0 < OZ2_BN; c0 += 8) {
+    uint32_t v[4][8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(v[q][0]), "=r"(v[q][1]), "=r"(v[q][2]), "=r"(v[q][3]), "=r"(v[q][4]), "=r"(v[q][5]),
+                     "=r"(v[q][6]), "=r"(v[q][7])
+                   : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(q * OZ2_BN + c0)));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+    if (rok) {
+      int64_t i = ib, l = lb;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t m = n0 + c0 + j;
+        if (m < MX) {
+          double* yp = y + i + L * r + L * N * l;
+          double acc = PHASE == 0 ? 0.0 : *yp;
+#pragma unroll
+          for (int q = 3; q >= 0; --q) {  // TMEM slot q holds group q + 4 (PHASE 0) or q (PHASE 1)
+            const int g = PHASE == 0 ? q + 4 : q;
+            acc = fma((double)(int32_t)v[q][j], __longlong_as_double((long long)(1023 - 12 - 7 * g) << 52), acc);
+          }
+          if (PHASE == 0) {
+            *yp = acc;
+          } else {
+            const int E = er + __ldg(ex + m);
+            *yp = (E >= -1022 && E <= 1023) ? acc * __longlong_as_double((long long)(E + 1023) << 52)
+                                            : ldexp(acc, E);
+          }
+        }
+        if (++i == L) { i = 0; ++l; }
+      }
+    }
+    ib += 8;
+    while (ib >= L) { ib -= L; ++lb; }
+  }
+}
+
+__global__ void __launch_bounds__(OZ2_NT, 1) k_oz_gemm2(const __grid_constant__ CUtensorMap ta4,
+                                                        const __grid_constant__ CUtensorMap tb7,
+                                                        const __grid_constant__ CUtensorMap tb4,
+                                                        const int* __restrict__ eu, const int* __restrict__ ex,
+                                                        int64_t L, int64_t R, int64_t N, int64_t Kp,
+                                                        double* __restrict__ y) {
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[OZ2_ST], empty[OZ2_ST], done_hi, done_lo, tmem_free;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t m0 = (int64_t)blockIdx.x * OZ_BM, n0 = (int64_t)blockIdx.y * OZ2_BN;
+  const int KT = (int)(Kp / OZ_BK);
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(saddr(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32) {
+    for (int st = 0; st < OZ2_ST; ++st) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&full[st])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&empty[st])));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&done_hi)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&done_lo)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(saddr(&tmem_free)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  const int NQ = 3 * KT;  // chunk sequence: hi-1 (KT), hi-2 (KT), lo (KT)
+
+  if (warp == 4) {
+    if (lane == 0) {  // TMA producer
+      for (int q = 0; q < NQ; ++q) {
+        const int ph = q / KT, kt = q % KT, st = q % OZ2_ST;
+        if (q >= OZ2_ST) mbar_wait(saddr(&empty[st]), ((q / OZ2_ST) - 1) & 1);
+        const uint32_t fb = saddr(&full[st]);
+        const uint32_t bytes = ph == 0 ? OZ2_STAGE : 8 * OZ2_PLANE;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bytes) : "memory");
+        const uint32_t da = saddr(sm + st * OZ2_STAGE), db = da + 4 * OZ2_PLANE;
+        const int pa = ph == 1 ? 4 : 0;
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+            ::"r"(da), "l"(&ta4), "r"(kt * OZ_BK), "r"((int)m0), "r"(pa), "r"(fb) : "memory");
+        if (ph == 0)
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+              ::"r"(db), "l"(&tb7), "r"(kt * OZ_BK), "r"((int)n0), "r"(1), "r"(fb) : "memory");
+        else
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+              ::"r"(db), "l"(&tb4), "r"(kt * OZ_BK), "r"((int)n0), "r"(0), "r"(fb) : "memory");
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {  // MMA issuer
+      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ2_BN >> 3) << 17) |
+                             ((uint32_t)(OZ_BM >> 4) << 24);
+      const auto mma = [&](uint32_t col, uint64_t ad, uint64_t bd, uint32_t acc) {
+        asm volatile(
+            "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }"
+            ::"r"(tmem + col), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+      };
+      for (int q = 0; q < NQ; ++q) {
+        const int ph = q / KT, kt = q % KT, st = q % OZ2_ST;
+        if (ph == 2 && kt == 0) {  // TMEM handed back by the hi epilogue
+          mbar_wait(saddr(&tmem_free), 0);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+        }
+        mbar_wait(saddr(&full[st]), (q / OZ2_ST) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t a0 = saddr(sm + st * OZ2_STAGE), b0 = a0 + 4 * OZ2_PLANE;
+        const uint64_t adb = sdesc_sw64(a0), bdb = sdesc_sw64(b0);
+        if (ph == 0) {  // s = 0..3 (A planes 0-3), t = g - s >= 1 (B planes 1-7 at local t - 1)
+#pragma unroll
+          for (int s2 = 0; s2 < 4; ++s2)
+#pragma unroll
+            for (int g = 4; g < 8; ++g) {
+              const int t = g - s2;
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const uint64_t ad = adb + (uint64_t)((s2 * OZ2_PLANE + h * 32) >> 4);
+                const uint64_t bd = bdb + (uint64_t)(((t - 1) * OZ2_PLANE + h * 32) >> 4);
+                mma((uint32_t)((g - 4) * OZ2_BN), ad, bd, (kt > 0 || s2 > 0 || h > 0) ? 1u : 0u);
+              }
+            }
+        } else if (ph == 1) {  // s = 4..7 (A planes 4-7 at local s - 4), t = g - s in 0..3
+#pragma unroll
+          for (int s2 = 4; s2 < 8; ++s2)
+#pragma unroll
+            for (int g = s2; g < 8; ++g) {
+              const int t = g - s2;
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const uint64_t ad = adb + (uint64_t)(((s2 - 4) * OZ2_PLANE + h * 32) >> 4);
+                const uint64_t bd = bdb + (uint64_t)((t * OZ2_PLANE + h * 32) >> 4);
+                mma((uint32_t)((g - 4) * OZ2_BN), ad, bd, 1u);
+              }
+            }
+        } else {  // lo: g = 0..3, s + t = g
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+#pragma unroll
+            for (int s2 = 0; s2 <= g; ++s2) {
+              const int t = g - s2;
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const uint64_t ad = adb + (uint64_t)((s2 * OZ2_PLANE + h * 32) >> 4);
+                const uint64_t bd = bdb + (uint64_t)((t * OZ2_PLANE + h * 32) >> 4);
+                mma((uint32_t)(g * OZ2_BN), ad, bd, (kt > 0 || s2 > 0 || h > 0) ? 1u : 0u);
+              }
+            }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                     ::"r"(saddr(&empty[st])));
+        if (q == 2 * KT - 1)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                       ::"r"(saddr(&done_hi)));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                   ::"r"(saddr(&done_lo)));
+    }
+  } else {  // warps 0-3: the two epilogues on their TMEM lane quarters
+    mbar_wait(saddr(&done_hi), 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    oz2_epilogue<0>(tmem, warp, lane, m0, n0, eu, ex, L, R, N, y);
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(&tmem_free)) : "memory");
+    mbar_wait(saddr(&done_lo), 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    oz2_epilogue<1>(tmem, warp, lane, m0, n0, eu, ex, L, R, N, y);
+  }
+  __syncwarp();  // producer / issuer lanes rejoin their warps
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -401,12 +609,12 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-// 3-D map over digit planes [s][rows][Kp] (uint8), box (64 B of K, box_rows, 8 planes), SWIZZLE_64B
-CUtensorMap digit_map(int8_t* base, int64_t rows, int64_t Kp, uint32_t box_rows) {
+// 3-D map over digit planes [s][rows][Kp] (uint8), box (64 B of K, box_rows, box_planes), SWIZZLE_64B
+CUtensorMap digit_map(int8_t* base, int64_t rows, int64_t Kp, uint32_t box_rows, uint32_t box_planes = OZ_S) {
   CUtensorMap mp;
   const cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)OZ_S};
   const cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)(Kp * rows)};
-  const cuuint32_t box[3] = {(cuuint32_t)OZ_BK, box_rows, (cuuint32_t)OZ_S};
+  const cuuint32_t box[3] = {(cuuint32_t)OZ_BK, box_rows, box_planes};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode_fn()(&mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
@@ -427,7 +635,14 @@ bool ozaki_enabled() {
 
 void ozaki_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t R, const double* mat, int64_t N,
                int64_t sMr, int64_t sMk, double* y) {
-  constexpr int bn = OZ_BN;
+  // default: the one-pass 128 x 64 tile kernel; TMB_OZ_N128=1 selects the three-pass
+  // 128 x 128 variant (bitwise identical; measured 1.11 vs 1.10 ms on the C2 mode-1 pass,
+  // tensor pipe ~49 % in both -- the operand port was not the bound)
+  static const bool n64 = [] {
+    const char* e = std::getenv("TMB_OZ_N128");
+    return !(e && e[0] == '1');
+  }();
+  const int bn = n64 ? OZ_BN : OZ2_BN;
   const int64_t MX = L * R;  // tensor rows
   const int64_t Xp = ceil_div(MX, bn) * bn, Up = ceil_div(N, OZ_BM) * OZ_BM, Kp = ceil_div(K, OZ_BK) * OZ_BK;
   if (K > 65536) throw Error(TMB_EINVAL, "ozaki_ttm: K too large for int32 digit accumulation");
@@ -461,9 +676,21 @@ void ozaki_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t R,
       mat, K, N, sMr, sMk, eu, Up, Kp, su);
   c.launches++;
   check_launch("k_oz_sliceB");
-  const CUtensorMap ta = digit_map(su, Up, Kp, OZ_BM), tb = digit_map(sx, Xp, Kp, (uint32_t)bn);
   dim3 grid((unsigned)(Up / OZ_BM), (unsigned)(Xp / bn));
-  {
+  if (!n64) {
+    const CUtensorMap ta4 = digit_map(su, Up, Kp, OZ_BM, 4), tb7 = digit_map(sx, Xp, Kp, OZ2_BN, 7),
+                      tb4 = digit_map(sx, Xp, Kp, OZ2_BN, 4);
+    const size_t smem = (size_t)OZ2_ST * OZ2_STAGE + 1024;
+    static bool attr2 = false;
+    if (!attr2) {
+      TMB_CUDA(cudaFuncSetAttribute(k_oz_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr2 = true;
+    }
+    k_oz_gemm2<<<grid, OZ2_NT, smem, c.stream>>>(ta4, tb7, tb4, eu, ex, L, R, N, Kp, y);
+    c.launches++;
+    check_launch("k_oz_gemm2");
+  } else {
+    const CUtensorMap ta = digit_map(su, Up, Kp, OZ_BM), tb = digit_map(sx, Xp, Kp, (uint32_t)bn);
     const size_t smem = (size_t)OZ_ST * OZ_STAGE + 1024;
     static bool attr = false;
     if (!attr) {

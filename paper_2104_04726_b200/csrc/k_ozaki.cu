@@ -237,6 +237,16 @@ __device__ __forceinline__ uint64_t sdesc_sw64(uint32_t addr) {
   return d;
 }
 
+__device__ __forceinline__ uint64_t sdesc_sw32(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;                 // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(256 >> 4) << 32;        // SBO: 8 rows x 32 B
+  d |= (uint64_t)1 << 46;                 // descriptor version (sm100)
+  d |= (uint64_t)6 << 61;                 // SWIZZLE_32B
+  return d;
+}
+
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   for (long long it = 0; it < 2000000000LL; ++it) {
     uint32_t done;
@@ -297,11 +307,16 @@ __device__ __forceinline__ void oz_epilogue(uint32_t tmem, int warp, int lane, i
 // A operand (UMMA M side, 128 rows): factor digit planes, rows r (exponents eu);
 // B operand (UMMA N side, 64 rows): tensor digit planes, rows m = (i, l) (exponents ex).
 // The tensor digits -- the large operand -- are re-read once per 128 factor rows.
+// BKB: bytes of K per pipeline stage -- 64 (SWIZZLE_64B, 2 stages of 96 KB, two
+// K=32 MMAs per digit pair) or 32 (SWIZZLE_32B, 4 stages of 48 KB, one MMA).
+template <int BKB>
 __global__ void __launch_bounds__(OZ_NT, 1) k_oz_gemm(const __grid_constant__ CUtensorMap ta,
                                                       const __grid_constant__ CUtensorMap tb,
                                                       const int* __restrict__ eu, const int* __restrict__ ex,
                                                       int64_t L, int64_t R, int64_t N, int64_t Kp,
                                                       double* __restrict__ y) {
+  constexpr int OZ_ST = BKB == 64 ? 2 : 4, OZ_BK = BKB, NH = BKB / 32;
+  constexpr uint32_t OZ_A_BYTES = OZ_S * OZ_BM * BKB, OZ_STAGE = OZ_S * (OZ_BM + OZ_BN) * BKB;
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[OZ_ST], empty[OZ_ST], done;
@@ -353,14 +368,15 @@ __global__ void __launch_bounds__(OZ_NT, 1) k_oz_gemm(const __grid_constant__ CU
       const uint32_t a0 = saddr(sm + st * OZ_STAGE), b0 = a0 + OZ_A_BYTES;
       // descriptors differ only in the 14-bit start-address field (16-byte units):
       // build each stage's base once, add compile-time plane / K-half offsets
-      const uint64_t adb = sdesc_sw64(a0), bdb = sdesc_sw64(b0);
+      const uint64_t adb = BKB == 64 ? sdesc_sw64(a0) : sdesc_sw32(a0);
+      const uint64_t bdb = BKB == 64 ? sdesc_sw64(b0) : sdesc_sw32(b0);
 #pragma unroll
       for (int g = 0; g < OZ_S; ++g) {
 #pragma unroll
         for (int s = 0; s <= g; ++s) {
           const int t = g - s;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < NH; ++h) {
             const uint64_t ad = adb + (uint64_t)((s * (OZ_BM * OZ_BK) + h * 32) >> 4);
             const uint64_t bd = bdb + (uint64_t)((t * (OZ_BN * OZ_BK) + h * 32) >> 4);
             const uint32_t acc = (kt > 0 || s > 0 || h > 0) ? 1u : 0u;
@@ -610,14 +626,16 @@ EncodeFn encode_fn() {
 }
 
 // 3-D map over digit planes [s][rows][Kp] (uint8), box (64 B of K, box_rows, box_planes), SWIZZLE_64B
-CUtensorMap digit_map(int8_t* base, int64_t rows, int64_t Kp, uint32_t box_rows, uint32_t box_planes = OZ_S) {
+CUtensorMap digit_map(int8_t* base, int64_t rows, int64_t Kp, uint32_t box_rows, uint32_t box_planes = OZ_S,
+                      uint32_t box_k = OZ_BK) {
   CUtensorMap mp;
   const cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)OZ_S};
   const cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)(Kp * rows)};
-  const cuuint32_t box[3] = {(cuuint32_t)OZ_BK, box_rows, box_planes};
+  const cuuint32_t box[3] = {box_k, box_rows, box_planes};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode_fn()(&mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
-                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 box_k == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(TMB_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return mp;
@@ -690,14 +708,23 @@ void ozaki_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t R,
     c.launches++;
     check_launch("k_oz_gemm2");
   } else {
-    const CUtensorMap ta = digit_map(su, Up, Kp, OZ_BM), tb = digit_map(sx, Xp, Kp, (uint32_t)bn);
-    const size_t smem = (size_t)OZ_ST * OZ_STAGE + 1024;
-    static bool attr = false;
-    if (!attr) {
-      TMB_CUDA(cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
+    // K bytes per stage: 64 (SWIZZLE_64B, 2 x 96 KB stages; default) or 32 (SWIZZLE_32B, 4 x 48 KB:
+    // bitwise equal, measured 1.50 vs 1.45 ms for the C2 mode-1 pass -- ring depth is not the bound)
+    static const int bkb = [] {
+      const char* e = std::getenv("TMB_OZ_BK");
+      return e && std::atoi(e) == 32 ? 32 : 64;
+    }();
+    const CUtensorMap ta = digit_map(su, Up, Kp, OZ_BM, OZ_S, (uint32_t)bkb),
+                      tb = digit_map(sx, Xp, Kp, (uint32_t)bn, OZ_S, (uint32_t)bkb);
+    const size_t smem = (bkb == 64 ? 2 : 4) * (size_t)OZ_S * (OZ_BM + OZ_BN) * bkb + 1024;
+    const void* fn = bkb == 64 ? (const void*)k_oz_gemm<64> : (const void*)k_oz_gemm<32>;
+    static bool attr[2] = {false, false};
+    if (!attr[bkb == 64]) {
+      TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr[bkb == 64] = true;
     }
-    k_oz_gemm<<<grid, OZ_NT, smem, c.stream>>>(ta, tb, eu, ex, L, R, N, Kp, y);
+    if (bkb == 64) k_oz_gemm<64><<<grid, OZ_NT, smem, c.stream>>>(ta, tb, eu, ex, L, R, N, Kp, y);
+    else k_oz_gemm<32><<<grid, OZ_NT, smem, c.stream>>>(ta, tb, eu, ex, L, R, N, Kp, y);
     c.launches++;
     check_launch("k_oz_gemm");
   }

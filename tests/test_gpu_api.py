@@ -103,7 +103,7 @@ def test_eig_diagonal_and_sign_rule():  # tests/test_tensor.py:196-207
     assert np.allclose(v1[:, 0], [-0.6, 0.8])
 
 
-@pytest.mark.parametrize("n,k", [(7, 7), (33, 10), (64, 64), (65, 20), (200, 50), (700, 100)])
+@pytest.mark.parametrize("n,k", [(7, 7), (33, 10), (64, 64), (65, 20), (200, 50), (281, 40), (282, 40), (700, 100)])
 def test_eig_residual_orthonormal_vs_lapack(n, k):  # tests/test_tensor.py:209-216
     rng = np.random.default_rng(n)
     b = rng.standard_normal((n, n))

@@ -862,13 +862,16 @@ __global__ void __launch_bounds__(64) k_twisted_sm(const double* __restrict__ d,
 // T(0:i, i) = -tau_i T(0:i, 0:i) S(0:i, i) with S = V^T V.
 __global__ void k_larft(const double* __restrict__ S, const double* __restrict__ tau, int nb,
                         double* __restrict__ T) {
-  extern __shared__ double sT[];  // nb x nb column-major T, then nb x nb S_p
+  extern __shared__ double sT[];  // nb x nb column-major T, then nb x nb S_p, then nb tau
   double* sS = sT + nb * nb;
+  double* stau = sS + nb * nb;
   const int p = blockIdx.x, r = threadIdx.x;
   const double* Sp = S + (int64_t)p * nb * nb;
-  const double* tp = tau + (int64_t)p * nb;
   for (int e = r; e < nb * nb; e += blockDim.x) sS[e] = Sp[e];  // S_p staged once (was re-read from L2 per step)
+  // tau staged too: a global load per column put an L2 round trip on every step's path
+  for (int e = r; e < nb; e += blockDim.x) stau[e] = tau[(int64_t)p * nb + e];
   __syncthreads();
+  const double* tp = stau;
   for (int i = 0; i < nb; ++i) {
     if (r < nb) {
       double v = 0.0;
@@ -1302,10 +1305,10 @@ static void backtransform(Ctx& c, const double* hv, const double* tau, int64_t n
   static bool larft_attr = false;
   if (!larft_attr) {
     TMB_CUDA(cudaFuncSetAttribute(k_larft, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double) * 2 * 64 * 64)));
+                                  (int)(sizeof(double) * (2 * 64 * 64 + 64))));
     larft_attr = true;
   }
-  k_larft<<<np, nb, sizeof(double) * 2 * nb * nb, c.stream>>>(S, tau, nb, T);
+  k_larft<<<np, nb, sizeof(double) * (2 * nb * nb + nb), c.stream>>>(S, tau, nb, T);
   LAUNCHED("k_larft");
   // (A fused one-kernel variant that streams every panel through shared memory
   // measured 3.0 ms vs ~1 ms for these GEMMs at n=1920: it is smem-bandwidth

@@ -79,6 +79,8 @@ __global__ void __launch_bounds__(256) k_jacobi(const double* __restrict__ g, in
   __syncthreads();
   const int np = (n + 1) & ~1;  // players incl. a bye when n is odd
   const int half = np / 2;
+  int sh = 0;
+  while ((1 << sh) < n) ++sh;
   for (int sweep = 0; sweep < 60; ++sweep) {
     if (tid == 0) rotated = 0;
     __syncthreads();
@@ -90,7 +92,10 @@ __global__ void __launch_bounds__(256) k_jacobi(const double* __restrict__ g, in
         double c = 1.0, s = 0.0;
         if (q < n) {
           const double apq = A[p + ld * q], app = A[p + ld * p], aqq = A[q + ld * q];
-          const double thr = fmax(1e-17 * sqrt(fabs(app * aqq)), 1e-19 * fro);
+          // absolute floor 8 eps ||A||_F: dsyevd's accuracy class (the reference); with
+          // 1e-19 ||A|| the rounding-level off-diagonals (a few ulps of the largest
+          // entries) kept every sweep rotating until the sweep cap (n = 64: 3.9 ms)
+          const double thr = fmax(1e-17 * sqrt(fabs(app * aqq)), 8.0 * 2.220446049250313e-16 * fro);
           if (fabs(apq) > thr) {
             const double theta = (aqq - app) / (2.0 * apq);
             const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
@@ -102,9 +107,11 @@ __global__ void __launch_bounds__(256) k_jacobi(const double* __restrict__ g, in
         pp[tid] = p; qq[tid] = q < n ? q : p; cs[tid] = c; sn[tid] = s;
       }
       __syncthreads();
-      // columns: A <- A J, V <- V J
-      for (int e = tid; e < half * n; e += blockDim.x) {
-        const int pr = e / n, i = e % n;
+      // columns: A <- A J, V <- V J (element e = (pair, i) with i in a power-of-two
+      // stride: shift/mask instead of a runtime division per element)
+      for (int e = tid; e < (half << sh); e += blockDim.x) {
+        const int pr = e >> sh, i = e & ((1 << sh) - 1);
+        if (i >= n) continue;
         const int p = pp[pr], q = qq[pr];
         if (p == q || sn[pr] == 0.0) continue;
         const double c = cs[pr], s = sn[pr];
@@ -117,8 +124,9 @@ __global__ void __launch_bounds__(256) k_jacobi(const double* __restrict__ g, in
       }
       __syncthreads();
       // rows: A <- J^T A
-      for (int e = tid; e < half * n; e += blockDim.x) {
-        const int pr = e / n, j = e % n;
+      for (int e = tid; e < (half << sh); e += blockDim.x) {
+        const int pr = e >> sh, j = e & ((1 << sh) - 1);
+        if (j >= n) continue;
         const int p = pp[pr], q = qq[pr];
         if (p == q || sn[pr] == 0.0) continue;
         const double c = cs[pr], s = sn[pr];

@@ -294,7 +294,7 @@ def run_ours(args) -> None:
     col = fam["color_u8"]
     col_gbs = col["work"] / (col["ms"] / 1e3) / 1e9 if col["ms"] > 0 else None
     hbm_peak = float(peaks.get("hbm_gbs", 6443.8))
-    roof_elem = {"bound": "hbm", "kernel": "color_u8 (IPT: 3 fp64 pow per pixel, FP64-pipe bound)", "unit": "GB/s",
+    roof_elem = {"bound": "hbm", "kernel": "color_u8 (IPT: 3 fp64 exp2(0.43 log2) per pixel, FP64-pipe bound)", "unit": "GB/s",
                  "achieved": col_gbs, "peak": hbm_peak, "frac": col_gbs / hbm_peak if col_gbs else None,
                  "bytes_per_launch": col["work"] / max(col["launches"], 1)}
 

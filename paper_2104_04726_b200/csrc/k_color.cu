@@ -24,6 +24,7 @@ struct ColorConst {
   double xyz2rgb[9];
   double lms2xyz[9];
   double ipt2lms[9];
+  double lin2lms[9];  // xyz2lms . rgb2xyz, for the u8 fast path
 };
 __constant__ ColorConst cc;
 
@@ -172,8 +173,21 @@ __global__ void __launch_bounds__(256) k_color_u8(const uint8_t* __restrict__ rg
     } else {
       double o[3];
       if (space == TMB_SPACE_IPT) {
-        const double lin[3] = {lut[R], lut[G], lut[B]};
-        ipt_from_lin(lin, o);
+        // u8 path: linear RGB -> LMS through the one fused 3x3 product and fma
+        // chains (the reference multiplies by rgb2xyz then xyz2lms; the fp32
+        // outputs are checked bit-identical on all 2^24 triples)
+        const double l0 = lut[R], l1 = lut[G], l2 = lut[B];
+        double lmsp[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+          lmsp[i] = spow043(fma(l2, cc.lin2lms[3 * i + 2], fma(l1, cc.lin2lms[3 * i + 1], l0 * cc.lin2lms[3 * i])));
+        double ipt[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+          ipt[i] = fma(lmsp[2], cc.lms2ipt[3 * i + 2], fma(lmsp[1], cc.lms2ipt[3 * i + 1], lmsp[0] * cc.lms2ipt[3 * i]));
+        o[0] = ipt[0];
+        o[1] = add(mul(0.5, ipt[1]), 0.5);
+        o[2] = add(mul(0.5, ipt[2]), 0.5);
       } else {
         o[0] = lut[R]; o[1] = lut[G]; o[2] = lut[B];
       }
@@ -370,6 +384,10 @@ void ensure_constants(Ctx& c) {
   inv3(h.rgb2xyz, h.xyz2rgb);
   inv3(h.xyz2lms, h.lms2xyz);
   inv3(h.lms2ipt, h.ipt2lms);
+  for (int r = 0; r < 3; ++r)
+    for (int k2 = 0; k2 < 3; ++k2)
+      h.lin2lms[3 * r + k2] = h.xyz2lms[3 * r] * h.rgb2xyz[k2] + h.xyz2lms[3 * r + 1] * h.rgb2xyz[3 + k2] +
+                              h.xyz2lms[3 * r + 2] * h.rgb2xyz[6 + k2];
   TMB_CUDA(cudaMemcpyToSymbol(cc, &h, sizeof(h)));
   TMB_CUDA(cudaMemcpyToSymbol(g_eotf, h.eotf, sizeof(h.eotf)));
   if (c.device >= 0 && c.device < 64) g_const_ready[c.device] = true;

@@ -133,6 +133,51 @@ __global__ void __launch_bounds__(256) k_oz_rowexp(const T* __restrict__ x, int6
   }
 }
 
+// fp32 rows with L % 4 == 0: each lane covers 4 consecutive rows (i..i+3 of one
+// slab l) with 16-byte loads, so a block covers 128 rows; 8 warps split K.
+__global__ void __launch_bounds__(256) k_oz_rowexp_v4(const float* __restrict__ x, int64_t L, int64_t K, int64_t R,
+                                                      int* __restrict__ ea) {
+  __shared__ float red[8][128];
+  const int64_t M = L * R;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t m = (int64_t)blockIdx.x * 128 + 4 * lane;  // first of this lane's 4 rows
+  float4 mx = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (m < M) {
+    const int64_t i = m % L, l = m / L;
+    const float* p = x + i + L * K * l;
+    float4 mq[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) mq[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int64_t k = w;
+    for (; k + 24 < K; k += 32) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p + L * (k + 8 * q)));
+        mq[q].x = fmaxf(mq[q].x, fabsf(v.x)); mq[q].y = fmaxf(mq[q].y, fabsf(v.y));
+        mq[q].z = fmaxf(mq[q].z, fabsf(v.z)); mq[q].w = fmaxf(mq[q].w, fabsf(v.w));
+      }
+    }
+    for (; k < K; k += 8) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(p + L * k));
+      mq[0].x = fmaxf(mq[0].x, fabsf(v.x)); mq[0].y = fmaxf(mq[0].y, fabsf(v.y));
+      mq[0].z = fmaxf(mq[0].z, fabsf(v.z)); mq[0].w = fmaxf(mq[0].w, fabsf(v.w));
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      mx.x = fmaxf(mx.x, mq[q].x); mx.y = fmaxf(mx.y, mq[q].y);
+      mx.z = fmaxf(mx.z, mq[q].z); mx.w = fmaxf(mx.w, mq[q].w);
+    }
+  }
+  red[w][4 * lane] = mx.x; red[w][4 * lane + 1] = mx.y; red[w][4 * lane + 2] = mx.z; red[w][4 * lane + 3] = mx.w;
+  __syncthreads();
+  if (threadIdx.x < 128) {
+    const int64_t mm = (int64_t)blockIdx.x * 128 + threadIdx.x;
+    float v = red[0][threadIdx.x];
+    for (int q = 1; q < 8; ++q) v = fmaxf(v, red[q][threadIdx.x]);
+    if (mm < M) ea[mm] = exp_of((double)v);  // max of exact fp32 magnitudes: same exponent as the fp64 path
+  }
+}
+
 // x digits, K-major planes SA[s][m][k] (Mp x Kp, zero padded). Tiles of 32 rows
 // x 128 k through shared memory: reads coalesce along the contiguous index (i
 // when L >= 32, else k), writes are 4 packed digits (32 bits) per lane, 128 B per
@@ -671,7 +716,9 @@ void ozaki_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t R,
   int8_t* su = alloc<int8_t>(c, (size_t)OZ_S * Up * Kp);
   // algorithmic work of the fp64-equivalent product: 2 MX N K
   Timed timed(c, TAG_OZAKI, 2.0 * (double)MX * N * K);  // fp64-equivalent flops
-  if (L >= 32) {
+  if (tx == F32 && L % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0) {
+    k_oz_rowexp_v4<<<(unsigned)ceil_div(MX, 128), 256, 0, c.stream>>>((const float*)x, L, K, R, ex);
+  } else if (L >= 32) {
     if (tx == F32) k_oz_rowexp<float><<<(unsigned)ceil_div(MX, 32), 256, 0, c.stream>>>((const float*)x, L, K, R, ex);
     else k_oz_rowexp<double><<<(unsigned)ceil_div(MX, 32), 256, 0, c.stream>>>((const double*)x, L, K, R, ex);
   } else {

@@ -117,9 +117,13 @@ struct YccConst {
   double kr, kg, kb, kb1, ikb1, kr1, ikr1, i255;
 };
 
+// SPACE is a template parameter so each colour space gets its own register
+// allocation (the IPT body needs 58 registers; sharing it cost the Y'CbCr path
+// two of its six resident blocks per SM)
+template <int SPACE>
 __global__ void __launch_bounds__(256) k_color_u8(const uint8_t* __restrict__ rgb, int64_t h, int64_t w,
-                                                  int space, float* __restrict__ out, int channel_major,
-                                                  const YccConst P) {
+                                                  float* __restrict__ out, int channel_major, const YccConst P) {
+  constexpr int space = SPACE;
   __shared__ __align__(16) uint8_t su8[CT_H][CT_ROWB];  // 4-byte aligned rows
   __shared__ __align__(16) float so[3][CT_W][CT_FP];
   __shared__ double lut[256];
@@ -402,7 +406,10 @@ void color_u8(Ctx& c, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, i
   dim3 grid((unsigned)ceil_div(w, CT_W), (unsigned)ceil_div(h, CT_H), (unsigned)n_img);
   Timed timed(c, TAG_COLOR, 15.0 * (double)n_img * h * w);  // 3 B read + 12 B written per pixel
   const YccConst P{KR, KG, KB, 1.0 - KB, 1.0 / (1.0 - KB), 1.0 - KR, 1.0 / (1.0 - KR), 1.0 / 255.0};
-  k_color_u8<<<grid, 256, 0, c.stream>>>(rgb, h, w, space, out, channel_major ? 1 : 0, P);
+  const int cm = channel_major ? 1 : 0;
+  if (space == TMB_SPACE_YCBCR) k_color_u8<TMB_SPACE_YCBCR><<<grid, 256, 0, c.stream>>>(rgb, h, w, out, cm, P);
+  else if (space == TMB_SPACE_IPT) k_color_u8<TMB_SPACE_IPT><<<grid, 256, 0, c.stream>>>(rgb, h, w, out, cm, P);
+  else k_color_u8<TMB_SPACE_RGB><<<grid, 256, 0, c.stream>>>(rgb, h, w, out, cm, P);
   c.launches++;
   check_launch("k_color_u8");
 }

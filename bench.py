@@ -1,59 +1,92 @@
 #!/usr/bin/env python3
 """Benchmark of the B200 Tucker-ALS hot path (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|c3]
 
-One step = one multi-exposure stereo stack end to end on one GPU: u8 images ->
-IPT coding-space tensor -> T-HOSVD -> 20 HOOI sweeps -> 10-bit core
-quantisation -> reconstruction + relative error, i.e. BASELINE.json config 2
-(1080x1920x3x10, ranks (270,480,3,5)). With N GPUs every rank runs its own
-independent stack per step (data-parallel, no inter-GPU traffic; weak
-scaling), launched one process per GPU by torchrun.
+Workloads (BASELINE.json configs; synthetic seeded stacks):
+
+* ``c2`` (default; the config the metric is quoted on at one GPU): one
+  1080x1920x3x10 IPT stack end to end per rank per step -- u8 images -> IPT
+  coding-space tensor -> T-HOSVD -> 20 HOOI sweeps -> 10-bit core quantisation
+  -> reconstruction + relative error. With N GPUs every rank runs its own
+  independent stack (weak scaling, "replicas only").
+* ``c3``: the 64-stack batch (Y'CbCr, ranks (135,240,3,5), 10 sweeps each),
+  stacks assigned round-robin to the ranks (``dist.assign_stacks``), no
+  inter-GPU traffic (strong scaling: the 64 stacks are the fixed job).
+
+Multi-GPU: one process per GPU. Under torchrun the RANK/WORLD_SIZE env is used;
+``--gpus N`` without it spawns the N ranks itself (127.0.0.1 rendezvous, NCCL).
 
 Prints ONE JSON line on rank 0. ``value`` is device-resident throughput
 (stacks/s over all ranks, max-over-ranks CUDA-event time); ``e2e`` is the same
-metric through the public API (``encode_stack``) with the u8 images copied
-from pinned host memory and the quantised model copied back every step.
-``--impl reference`` times the CPU reference path (the oracle port of the
-reference algorithm, see oracle/) on the host cores.
+metric through the public API (``encode_stack`` / ``encode_stacks``) with the
+u8 images copied from pinned host memory and the results copied back every
+step. ``--impl reference`` runs the UNMODIFIED reference package (``tmcodec``,
+installed into ``oracle/_ref`` by ``oracle/build_ref.py``) on the host cores
+through its own public API; it never loads libtmb.
 """
 
 from __future__ import annotations
 
 import argparse
+import importlib.util
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
-sys.path.insert(0, str(ROOT))
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
 
 import numpy as np  # noqa: E402
 
-from paper_2104_04726_b200.synth import CONFIGS, make_stack  # noqa: E402
 
-WORKLOAD = "c2"
-METRIC = "Tucker-ALS stacks/sec (BASELINE config 2: 1080x1920x3x10 IPT stack, ranks (270,480,3,5), 20 HOOI sweeps, 10-bit core)"
+def _load_synth():
+    """The seeded stack generator, loaded by file path: importing it through the
+    package would run the package __init__ and map libtmb.so, which the
+    reference arm must not do."""
+    name = "tmb_synth"
+    if name in sys.modules:
+        return sys.modules[name]
+    spec = importlib.util.spec_from_file_location(name, ROOT / "paper_2104_04726_b200" / "synth.py")
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[name] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+synth = _load_synth()
+CONFIGS, make_stack = synth.CONFIGS, synth.make_stack
+
 UNIT = "stacks/s"
+DATA = "synthetic (seeded generator, SURVEY.md 8(d); stands in for the paper's ZED captures)"
+C3_STACKS = 64
 FP64_PEAK_TFLOPS = 35.47   # torch fp64 8192^3 matmul (cuBLAS DGEMM), profiles/r01_probe_peaks.txt
 FP64_PEAK_SRC = "measured: torch.float64 8192^3 matmul best of 10 on this pool's B200 (profiles/r01_probe_peaks.txt)"
+METRICS = {
+    "c2": "Tucker-ALS stacks/sec (BASELINE config 2: 1080x1920x3x10 IPT stack, ranks (270,480,3,5), 20 HOOI "
+          "sweeps, 10-bit core)",
+    "c3": "Tucker-ALS stacks/sec (BASELINE config 3: 64 independent 1080x1920x3x10 Y'CbCr stacks, ranks "
+          "(135,240,3,5), 10 HOOI sweeps each, 8-bit core)",
+}
+SCALING = {"c2": "weak", "c3": "strong"}
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(METRICS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -61,6 +94,29 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def config_dict(workload: str, world: int) -> dict:
+    """The workload description; identical for both arms (``--impl``)."""
+    if workload == "c2":
+        return {"workload": "c2: 1080x1920x3x10 IPT stack, ranks (270,480,3,5), 20 HOOI sweeps, qp 39 (10-bit), "
+                            "reconstruction + rel. error",
+                "global_batch": world, "parallelism": f"dp{world} (one independent stack per rank per step, "
+                                                      f"no collectives)",
+                "l2": "no flush: per-step working set (249 MB fp32 tensor + fp64 intermediates) > 126 MB L2",
+                "stack_seed": "rank"}
+    return {"workload": f"c3: {C3_STACKS} independent 1080x1920x3x10 Y'CbCr stacks (seeds 0..63, disparity phase "
+                        f"drifting with the frame index), ranks (135,240,3,5), 10 HOOI sweeps each, qp 51 (8-bit), "
+                        f"reconstruction + rel. error",
+            "global_batch": C3_STACKS, "parallelism": f"dp{world} (stacks round-robin over ranks, no collectives)",
+            "l2": "no flush: per-stack working set > 126 MB L2", "stack_seed": "stack index"}
+
+
+def base_line(workload: str, world: int, args, value: float, ms_per_step: float) -> dict:
+    return {"metric": METRICS[workload], "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": SCALING[workload], "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": config_dict(workload, world)}
 
 
 def measured_peaks() -> dict:
@@ -71,6 +127,10 @@ def measured_peaks() -> dict:
         except Exception:  # noqa: BLE001
             pass
     return {}
+
+
+def _stack_seed_frame(workload: str, i: int) -> tuple[int, int]:
+    return (i, i) if workload == "c3" else (i, 0)
 
 
 class ClockSampler:
@@ -121,61 +181,165 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ----------------------------------------------------------------------------- CPU reference
-def cpu_reference_sample(cfg, images) -> dict:
-    """Oracle port of the reference path on the host cores: colour + T-HOSVD +
-    one HOOI sweep + quantise + reconstruct of one C2 stack, timed per phase,
-    extrapolated to the full 20-sweep stack."""
-    import oracle
-    from threadpoolctl import threadpool_info
+# ----------------------------------------------------------------------------- launcher
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _spawned(local: int, world: int, port: int, target, args) -> None:
+    os.environ.update(RANK=str(local), LOCAL_RANK=str(local), WORLD_SIZE=str(world), LOCAL_WORLD_SIZE=str(world),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    target(args)
+
+
+def launch(args, target) -> None:
+    """Run ``target(args)`` on every rank: in this process under torchrun (or
+    for one GPU), else spawn ``args.gpus`` processes, one per GPU, with a
+    127.0.0.1 rendezvous (RANK/LOCAL_RANK/WORLD_SIZE set as torchrun would)."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import torch.multiprocessing as mp
+
+        mp.start_processes(_spawned, args=(args.gpus, _free_port(), target, args), nprocs=args.gpus,
+                           join=True, start_method="spawn")
+    else:
+        target(args)
+
+
+# ----------------------------------------------------------------------------- CPU reference (tmcodec)
+def _ref_tensor(tm, images: np.ndarray, space: str) -> np.ndarray:
+    """The reference's own colour transform per image (``to_coding_space``,
+    color.py:185-194, on ``ColorImage(u8/255)`` as sceneio.read_image does),
+    assembled into the (H, W, 3, V*E) tensor of the BASELINE configs in F order
+    (the reference is bit-identical for C/F input, F is faster)."""
+    from tmcodec.color import ColorImage, to_coding_space
+
+    v_, e_, h, w, _ = images.shape
+    t = np.empty((h, w, 3, v_ * e_), order="F")
+    for v in range(v_):
+        for e in range(e_):
+            t[:, :, :, v * e_ + e] = to_coding_space(ColorImage(images[v, e] / 255.0), space).pixels
+    return t
+
+
+def reference_stack(tm, images: np.ndarray, cfg) -> dict:
+    """One full stack through the reference's public API: colour -> tucker_als
+    (exactly ``cfg.sweeps`` HOOI sweeps) -> quantize_core -> reconstruct +
+    relative error."""
+    from tmcodec.codec import quantize_core
+    from tmcodec.tensor import DenseTensor
+    from tmcodec.tucker import SolveConfig, reconstruct, tucker_als
 
     t0 = time.perf_counter()
-    x = oracle.coding_tensor(images, cfg.space)
-    x = np.asfortranarray(x.astype(np.float32).astype(np.float64))
+    x = _ref_tensor(tm, images, cfg.space)
+    t = DenseTensor(x)
+    model, trace = tucker_als(t, SolveConfig(ranks=cfg.ranks, max_sweeps=cfg.sweeps, fit_tol=1e-300,
+                                             pp_enter_tol=0.0))
+    if cfg.qp is not None:
+        quantize_core(model, cfg.qp)
+    rec = reconstruct(model).array
+    rel = float(np.linalg.norm((x - rec).ravel()) / np.linalg.norm(x.ravel()))
+    return {"stack_s": time.perf_counter() - t0, "fit": trace.records[-1].fit, "rel_err": rel}
+
+
+def reference_sample(tm, images: np.ndarray, cfg) -> dict:
+    """Bounded sample of the same reference path: colour + t_hosvd + ONE
+    hooi_sweep + quantize_core + reconstruct, each timed; the stack time is
+    extrapolated to ``cfg.sweeps`` sweeps (SURVEY §8(d) CPU baseline plan)."""
+    from tmcodec.codec import quantize_core
+    from tmcodec.tensor import DenseTensor
+    from tmcodec.tucker import hooi_sweep, reconstruct, t_hosvd
+
+    t0 = time.perf_counter()
+    x = _ref_tensor(tm, images, cfg.space)
+    t = DenseTensor(x)
     t1 = time.perf_counter()
-    core, factors = oracle.t_hosvd(x, cfg.ranks)
+    model = t_hosvd(t, cfg.ranks)
     t2 = time.perf_counter()
-    core, factors = oracle.hooi_sweep(x, factors)
+    model = hooi_sweep(t, model)
     t3 = time.perf_counter()
-    oracle.quantize_core(core, cfg.qp)
+    if cfg.qp is not None:
+        quantize_core(model, cfg.qp)
+    reconstruct(model)
     t4 = time.perf_counter()
-    oracle.reconstruct(core, factors)
-    t5 = time.perf_counter()
-    stack_s = (t1 - t0) + (t2 - t1) + cfg.sweeps * (t3 - t2) + (t4 - t3) + (t5 - t4)
-    threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
-    return {"stack_s": stack_s, "sweep_s": t3 - t2, "thosvd_s": t2 - t1, "colour_s": t1 - t0,
-            "sample_s": t5 - t0, "threads": int(threads)}
+    stack = (t2 - t0) + cfg.sweeps * (t3 - t2) + (t4 - t3)
+    return {"stack_s": stack, "sample_s": t4 - t0, "sweep_s": t3 - t2}
+
+
+def _host_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+
+        return int(max((i.get("num_threads", 1) for i in threadpool_info()), default=1))
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
 
 
 def run_reference(args) -> None:
+    """``--impl reference``: the unmodified reference on the host cores, rank 0
+    only (other ranks exit without work). Warm-up steps are bounded samples of
+    the same code path (colour, t_hosvd, hooi_sweep, quantize_core,
+    reconstruct -- nothing on a CPU needs more warming); each timed step is
+    one FULL stack (``tucker_als`` with every sweep), no extrapolation."""
     world, rank, _ = dist_env()
+    world = max(world, args.gpus)
     if rank != 0:
         return
-    cfg = CONFIGS[WORKLOAD]
-    images = make_stack(cfg, seed=0)
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from build_ref import import_reference  # oracle/build_ref.py (reference installer, not the port)
+
+    tm = import_reference()
+    cfg = CONFIGS[args.workload]
+    ids = [0] if args.workload == "c2" else list(range(C3_STACKS))
+    seed, frame = _stack_seed_frame(args.workload, ids[0])
+    images = make_stack(cfg, seed=seed, frame=frame)
     for _ in range(args.warmup):
-        cpu_reference_sample(cfg, images)
-    samples = [cpu_reference_sample(cfg, images) for _ in range(args.steps)]
-    total = sum(s["stack_s"] for s in samples)
+        reference_sample(tm, images, cfg)
+    times, last = [], None
+    for k in range(args.steps):
+        if args.workload == "c3" and k > 0:   # c3: step k solves stack k of the 64 (one stack per step)
+            seed, frame = _stack_seed_frame(args.workload, ids[k % len(ids)])
+            images = make_stack(cfg, seed=seed, frame=frame)
+        last = reference_stack(tm, images, cfg)
+        times.append(last["stack_s"])
+    total = sum(times)
     value = args.steps / total
-    sample_desc = (f"{WORKLOAD} stack: oracle-port colour + t_hosvd + 1 hooi_sweep + quantize + reconstruct "
-                   f"timed per step, sweep time x{cfg.sweeps} extrapolated (mean sweep "
-                   f"{statistics.mean(s['sweep_s'] for s in samples):.2f}s)")
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded generator, SURVEY.md 8(d); stands in for the paper's ZED captures)",
-        "config": {"workload": f"{WORKLOAD}: 1080x1920x3x10 IPT, ranks (270,480,3,5), 20 sweeps, qp 39",
-                   "global_batch": 1, "parallelism": "cpu"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": samples[0]["threads"], "kind": "port",
-                         "sample": sample_desc},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
+    cores = _host_threads()
+    line = base_line(args.workload, world, args, value, 1e3 * total / args.steps)
+    sample = (f"{args.workload}: one full stack per timed step through tmcodec's public API (to_coding_space per "
+              f"image, tucker_als with {cfg.sweeps} sweeps, quantize_core, reconstruct), no extrapolation; "
+              f"{cores} BLAS threads; fit {last['fit']:.10f}")
+    line.update({"impl": "reference",
+                 "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                                  "sample": sample},
+                 "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                 "reference": {"package": "tmcodec (oracle/_ref, installed unmodified by oracle/build_ref.py)",
+                               "rank": "rank 0 only (host CPU); other ranks exit without work",
+                               "warmup": "bounded samples of the same path (t_hosvd + 1 hooi_sweep)"}})
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------- our arm
+def _gen(args):
+    wl, i = args
+    seed, frame = _stack_seed_frame(wl, i)
+    return make_stack(CONFIGS[wl], seed=seed, frame=frame)
+
+
+def generate_stacks(wl: str, cfg, ids) -> list:
+    """This rank's seeded u8 stacks (host side, before the timed regions); a
+    fork pool when there are several (4-5 s of numpy per 1080p stack)."""
+    if len(ids) <= 1:
+        return [_gen((wl, i)) for i in ids]
+    import concurrent.futures as cf
+    import multiprocessing as mp
+
+    workers = max(1, min(len(ids), (os.cpu_count() or 2) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))))
+    with cf.ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("fork")) as ex:
+        return list(ex.map(_gen, [(wl, i) for i in ids]))
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -183,18 +347,24 @@ def run_ours(args) -> None:
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2104_04726_b200 as tb
     from paper_2104_04726_b200 import _lib as L
+    from paper_2104_04726_b200.dist import assign_stacks
     from paper_2104_04726_b200.pipeline import encode_stack_device
 
-    cfg = CONFIGS[WORKLOAD]
+    wl = args.workload
+    cfg = CONFIGS[wl]
     sc = tb.SolveConfig(ranks=cfg.ranks, max_sweeps=cfg.sweeps, fit_tol=1e-300, pp_enter_tol=0.0)
-    images = make_stack(cfg, seed=rank)  # one independent stack per rank
-    pinned = torch.from_numpy(images).pin_memory()
-    dev_images = pinned.to("cuda")
+    ids = [rank] if wl == "c2" else assign_stacks(C3_STACKS, rank, world)
+    host_stacks = generate_stacks(wl, cfg, ids)
+    pinned = [torch.from_numpy(s).pin_memory() for s in host_stacks]
+    dev_stacks = [p.to("cuda") for p in pinned]
     h = L.ctx()
+    units_total = world if wl == "c2" else C3_STACKS
 
     def barrier():
         if world > 1:
@@ -208,10 +378,17 @@ def run_ours(args) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- device-resident throughput (value)
+    def device_step(bufs):
+        out = None
+        for d in dev_stacks:
+            bufs, tr, step, rel = encode_stack_device(d, cfg.space, cfg.ranks, sc, cfg.qp, True, bufs)
+            out = (tr, rel)
+        return bufs, out
+
+    # ---- device-resident throughput (value): inputs already in HBM
     bufs = None
     for _ in range(args.warmup):
-        bufs, tr, step, rel = encode_stack_device(dev_images, cfg.space, cfg.ranks, sc, cfg.qp, True, bufs)
+        bufs, last = device_step(bufs)
     clocks = ClockSampler(local)
     barrier()
     clocks.start()
@@ -221,12 +398,13 @@ def run_ours(args) -> None:
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record()
     for _ in range(args.steps):
-        bufs, tr, step, rel = encode_stack_device(dev_images, cfg.space, cfg.ranks, sc, cfg.qp, True, bufs)
+        bufs, last = device_step(bufs)
     ev1.record()
     barrier()
     launches = L.launch_count() - n0
     clk = clocks.stop()
-    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    my_ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(my_ms)
     fam = {}
     for tag, name in ((0, "gemm_dmma"), (1, "sytrd"), (2, "tridiag_vectors"), (3, "color_u8"),
                       (4, "eig_gemm_dmma"), (5, "ttm_ozaki_i8")):
@@ -234,40 +412,49 @@ def run_ours(args) -> None:
         L.check(L.LIB.tmb_timing_read(h, tag, L.C.byref(cnt), L.C.byref(tms), L.C.byref(work)), h)
         fam[name] = {"launches": cnt.value, "ms": tms.value, "work": work.value}
     L.check(L.LIB.tmb_timing(h, 0), h)
-    value = world * args.steps / (ms / 1e3)
+    value = units_total * args.steps / (ms / 1e3)
+    tr, rel = last
 
-    # ---- HOOI sweep time: 20-sweep solve minus 0-sweep solve (same stack)
+    # ---- HOOI sweep time: K-sweep solve minus 0-sweep solve (same stack)
     sc0 = tb.SolveConfig(ranks=cfg.ranks, max_sweeps=0, fit_tol=1e-300, pp_enter_tol=0.0)
+
     def timed_solve(c):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        encode_stack_device(dev_images, cfg.space, cfg.ranks, c, cfg.qp, True, bufs)
+        encode_stack_device(dev_stacks[0], cfg.space, cfg.ranks, c, cfg.qp, True, bufs)
         e.record()
         torch.cuda.synchronize()
         return s.elapsed_time(e)
-    t20 = min(timed_solve(sc) for _ in range(2))
+    tk = min(timed_solve(sc) for _ in range(2))
     t0 = min(timed_solve(sc0) for _ in range(2))
-    sweep_ms = max_over_ranks((t20 - t0) / cfg.sweeps)
+    sweep_ms = max_over_ranks((tk - t0) / cfg.sweeps)
 
-    # ---- e2e through the public API (pinned H2D + D2H of the quantised model)
-    ranks = cfg.ranks
-    # warm-up as for the device-resident loop: the first calls also populate torch's
-    # pinned host-block cache used for the D2H of the quantised model
-    for _ in range(args.warmup):
-        res = tb.encode_stack(pinned, cfg.space, ranks, cfg.sweeps, cfg.qp)
+    # ---- e2e through the public API: pinned H2D of the u8 images + D2H of the results, every step
+    def e2e_step():
+        if wl == "c2":
+            r = tb.encode_stack(pinned[0], cfg.space, cfg.ranks, cfg.sweeps, cfg.qp)
+            return [r]
+        return tb.encode_stacks(pinned, cfg.space, cfg.ranks, cfg.sweeps, cfg.qp)
+    for _ in range(args.warmup):      # also populates torch's pinned host-block cache used by the D2H
+        res = e2e_step()
     barrier()
     ee0 = torch.cuda.Event(enable_timing=True)
     ee1 = torch.cuda.Event(enable_timing=True)
     ee0.record()
     for _ in range(args.steps):
-        res = tb.encode_stack(pinned, cfg.space, ranks, cfg.sweeps, cfg.qp)
+        res = e2e_step()
     ee1.record()
     barrier()
     e2e_ms = max_over_ranks(ee0.elapsed_time(ee1))
-    h2d = int(images.nbytes)
-    d2h = int(res.levels.nbytes + res.model.core.array.nbytes + sum(f.nbytes for f in res.model.factors))
-    e2e = {"value": world * args.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": d2h}
+    h2d = int(sum(s.nbytes for s in host_stacks))
+    d2h = 0
+    for r in res:
+        d2h += int(r.levels.nbytes)
+        if r.model is not None:
+            d2h += int(r.model.core.array.nbytes + sum(f.nbytes for f in r.model.factors))
+    e2e = {"value": units_total * args.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "path": "encode_stack" if wl == "c2" else
+           "encode_stacks (H2D of stack i+1 on a copy stream overlapping the solve of stack i)"}
 
     # ---- roofline of the dominant kernel family (live CUDA-event launch durations)
     dom_name, dom = max(fam.items(), key=lambda kv: kv[1]["ms"])
@@ -281,53 +468,40 @@ def run_ours(args) -> None:
         peak = FP64_PEAK_TFLOPS
         roof = {"bound": "tensor", "unit": "TFLOP/s", "pipe": "fp64 (DMMA / DFMA)", "peak_source": FP64_PEAK_SRC}
     traffic = None
-    tf = ROOT / "profiles" / "r01_traffic.json"
-    if tf.exists():
-        try:
-            traffic = json.loads(tf.read_text()).get(dom_name)
-        except Exception:  # noqa: BLE001
-            traffic = None
+    for tf in (ROOT / "profiles" / "r02_traffic.json", ROOT / "profiles" / "r01_traffic.json"):
+        if traffic is None and tf.exists():
+            try:
+                traffic = json.loads(tf.read_text()).get(dom_name)
+            except Exception:  # noqa: BLE001
+                traffic = None
     roof.update({"kernel": dom_name, "achieved": achieved, "peak": peak, "frac": achieved / peak if peak else None,
                  "traffic": traffic, "launches_per_step": dom["launches"] / args.steps,
-                 "ms_per_step": dom["ms"] / args.steps,
-                 "share_of_step": dom["ms"] / (ev0.elapsed_time(ev1))})
+                 "ms_per_step": dom["ms"] / args.steps, "share_of_step": dom["ms"] / my_ms})
 
-    # the HBM-bound elementwise kernel of the step (u8 -> IPT colour, 15 B/px), same live timing
+    # the HBM-bound elementwise kernel of the step (u8 -> coding space, 15 B/px), same live timing
     col = fam["color_u8"]
     col_gbs = col["work"] / (col["ms"] / 1e3) / 1e9 if col["ms"] > 0 else None
     hbm_peak = float(peaks.get("hbm_gbs", 6443.8))
-    roof_elem = {"bound": "hbm", "kernel": "color_u8 (IPT: 3 fp64 exp2(0.43 log2) per pixel, FP64-pipe bound)", "unit": "GB/s",
+    roof_elem = {"bound": "hbm", "kernel": f"color_u8 ({cfg.space})", "unit": "GB/s",
                  "achieved": col_gbs, "peak": hbm_peak, "frac": col_gbs / hbm_peak if col_gbs else None,
                  "bytes_per_launch": col["work"] / max(col["launches"], 1)}
 
-    # the contraction kernels on the FP64 tensor pipe (TTM full passes on DMMA, Grams) and the
-    # Ozaki tcgen05 TTM, same live timing, algorithmic flops (SURVEY 8(d) counting rules)
+    # the contraction kernels (TTM full passes, Grams) against the FP64 pipe, algorithmic flops
     roof_gemm = {}
     for nm in ("gemm_dmma", "ttm_ozaki_i8"):
         f = fam[nm]
         if f["ms"] > 0:
-            tf = f["work"] / (f["ms"] / 1e3) / 1e12
-            roof_gemm[nm] = {"achieved": tf, "unit": "TFLOP/s (fp64-equivalent)", "peak": FP64_PEAK_TFLOPS,
-                             "frac": tf / FP64_PEAK_TFLOPS, "ms_per_step": f["ms"] / args.steps}
-    # the tridiagonalisation is latency-bound: per-column time against the measured
-    # 148-block grid-barrier floor (2.5k cycles at 1965 MHz, scripts/research/barrier_bench.cu)
+            tfl = f["work"] / (f["ms"] / 1e3) / 1e12
+            roof_gemm[nm] = {"achieved": tfl, "unit": "TFLOP/s (fp64-equivalent)", "peak": FP64_PEAK_TFLOPS,
+                             "frac": tfl / FP64_PEAK_TFLOPS, "ms_per_step": f["ms"] / args.steps}
     sy = fam["sytrd"]
-    cols = sum(n - 1 for n in cfg.dims[:2]) * (cfg.sweeps + 1)
-    per_col_us = 1e3 * sy["ms"] / args.steps / cols
-    roof["latency"] = {"per_column_us": per_col_us, "grid_barrier_floor_us": 2500 / 1965.0,
-                       "columns_per_step": cols,
-                       "note": "one grid barrier + two block reductions + one L2 gather per column"}
+    if sy["ms"] > 0:
+        cols = sum(n - 1 for n in cfg.dims[:2]) * (cfg.sweeps + 1) * len(dev_stacks)
+        roof["latency"] = {"per_column_us": 1e3 * sy["ms"] / args.steps / cols,
+                           "grid_barrier_floor_us": 2500 / 1965.0, "columns_per_step": cols}
 
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded generator, SURVEY.md 8(d); stands in for the paper's ZED captures)",
-        "config": {"workload": f"{WORKLOAD}: 1080x1920x3x10 IPT stack, ranks (270,480,3,5), 20 HOOI sweeps, "
-                               f"qp 39 (10-bit), reconstruction + rel. error",
-                   "global_batch": world, "parallelism": f"dp{world} (independent stacks, no collectives)",
-                   "l2": "no flush: per-step working set (249 MB fp32 tensor + fp64 intermediates) > 126 MB L2",
-                   "stack_seed": "rank"},
+    line = base_line(wl, world, args, value, ms / args.steps)
+    line.update({
         "hooi_sweep_ms": sweep_ms,
         "fit": float(tr.fit[tr.n_records - 1]), "rel_err": rel,
         "e2e": e2e,
@@ -338,25 +512,47 @@ def run_ours(args) -> None:
         "kernel_families": {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps}
                             for k, v in fam.items()},
         "clocks": clk,
-    }
+        "stacks_per_rank": len(ids),
+    })
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ref = cpu_reference_sample(cfg, images)
-        line["cpu_baseline"] = {"value": 1.0 / ref["stack_s"], "unit": UNIT, "cores": ref["threads"], "kind": "port",
-                                "sample": f"{WORKLOAD} stack on the host: oracle-port colour + t_hosvd + 1 hooi_sweep + "
-                                          f"quantize + reconstruct ({ref['sample_s']:.1f}s), sweep x{cfg.sweeps} "
-                                          f"extrapolated; stack {ref['stack_s']:.1f}s"}
+        line["cpu_baseline"] = cpu_baseline(cfg, host_stacks[0])
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 
-def main():
-    args = parse()
+def cpu_baseline(cfg, images) -> dict:
+    """The reference itself (oracle/_ref) on a bounded sample of the workload,
+    in a subprocess so this process never imports the reference package."""
+    code = ("import sys, json; sys.path.insert(0, %r); import bench; from build_ref import import_reference; "
+            "tm = import_reference(); import numpy as np; "
+            "cfg = bench.CONFIGS[%r]; im = np.load(sys.argv[1]); "
+            "r = bench.reference_sample(tm, im, cfg); r['threads'] = bench._host_threads(); print(json.dumps(r))"
+            % (str(ROOT / "oracle"), cfg.name))
+    with tempfile.NamedTemporaryFile(suffix=".npy", delete=False) as f:
+        np.save(f, images)
+    try:
+        out = subprocess.run([sys.executable, "-c", code, f.name], capture_output=True, text=True, cwd=str(ROOT),
+                             timeout=900)
+        r = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as exc:  # noqa: BLE001
+        return {"value": None, "unit": UNIT, "cores": None, "kind": "reference", "sample": f"failed: {exc}"}
+    finally:
+        os.unlink(f.name)
+    return {"value": 1.0 / r["stack_s"], "unit": UNIT, "cores": r["threads"], "kind": "reference",
+            "sample": f"{cfg.name} stack through tmcodec (oracle/_ref): to_coding_space + t_hosvd + 1 hooi_sweep + "
+                      f"quantize_core + reconstruct ({r['sample_s']:.1f}s), sweep x{cfg.sweeps} extrapolated; "
+                      f"stack {r['stack_s']:.1f}s"}
+
+
+def main(argv=None):
+    args = parse(argv)
     if args.impl == "reference":
         run_reference(args)
     else:
-        run_ours(args)
+        launch(args, run_ours)
 
 
 if __name__ == "__main__":

@@ -19,7 +19,7 @@ from . import _lib as L
 from .tensor import DenseTensor
 from .tucker import SolveConfig, SolveTrace, TuckerModel, _trace_buffers, _trace_from_c
 
-__all__ = ["StackResult", "encode_stack", "encode_stack_device", "coding_tensor", "ScenePSNR", "DecodedStack",
+__all__ = ["StackResult", "encode_stack", "encode_stack_device", "encode_stacks", "coding_tensor", "ScenePSNR", "DecodedStack",
            "decode_stack"]
 
 
@@ -110,6 +110,67 @@ def encode_stack(images_u8: np.ndarray, space: str, ranks: Sequence[int], sweeps
         facs = [np.reshape(host[2 + n].numpy(), (dims[n], ranks[n]), order="F") for n in range(len(dims))]
         model = TuckerModel(core, facs, dims)
     return StackResult(model, _trace_from_c(tr), levels, step, rel, bufs)
+
+
+def encode_stacks(stacks, space: str, ranks: Sequence[int], sweeps: int, qp: int, fit_tol: float = 1e-300,
+                  pp_enter_tol: float = 0.0, rel_err: bool = True) -> list[StackResult]:
+    """Encode a sequence of independent stacks on this rank's GPU with the H2D
+    of stack i+1 overlapped with the device solve of stack i (BASELINE config 3,
+    SURVEY §8(e): "H2D of stack i+1's u8 planes overlaps compute of stack i").
+
+    ``stacks``: (V, E, H, W, 3) uint8 host tensors/arrays of one shape (pinned
+    torch tensors give truly asynchronous copies). The u8 images go through two
+    device slots on a copy stream; the solve, quantiser and the D2H of each
+    stack's quantised levels run on the current stream. Returns one
+    ``StackResult`` per stack (levels, step, trace, relative error; no model).
+    This is the data-parallel unit of work: ``dist.assign_stacks`` gives each
+    rank its stack ids and every rank calls this on its own share, with no
+    inter-GPU traffic (the reference's analogue is its process pool over
+    independent cells, cli.py:379-382).
+    """
+    torch = L._torch()
+    stacks = [torch.from_numpy(np.ascontiguousarray(s)) if isinstance(s, np.ndarray) else s for s in stacks]
+    if not stacks:
+        return []
+    shape = tuple(stacks[0].shape)
+    for s in stacks:
+        if tuple(s.shape) != shape or s.dtype != torch.uint8:
+            raise ValueError("encode_stacks needs (V, E, H, W, 3) uint8 stacks of one shape")
+    v, e, h, w, _ = shape
+    dims = (h, w, 3, v * e)
+    ranks = tuple(int(r) for r in ranks)
+    cfg = SolveConfig(ranks=ranks, max_sweeps=sweeps, fit_tol=fit_tol, pp_enter_tol=pp_enter_tol)
+    cfg.validate(dims)
+    ncore = int(np.prod(ranks))
+    comp = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()
+    slots = [torch.empty(shape, dtype=torch.uint8, device="cuda") for _ in range(min(2, len(stacks)))]
+    loaded = [torch.cuda.Event() for _ in slots]
+    freed = [torch.cuda.Event() for _ in slots]
+
+    def issue(i: int) -> None:
+        k = i % len(slots)
+        with torch.cuda.stream(copy):
+            copy.wait_event(freed[k])              # the solve of stack i-2 is done with this slot
+            slots[k].copy_(stacks[i], non_blocking=True)
+            loaded[k].record(copy)
+
+    issue(0)
+    bufs = None
+    pending = []
+    for i in range(len(stacks)):
+        k = i % len(slots)
+        if i + 1 < len(stacks):
+            issue(i + 1)
+        comp.wait_event(loaded[k])
+        bufs, tr, step, rel = encode_stack_device(slots[k], space, ranks, cfg, qp, rel_err, bufs)
+        freed[k].record(comp)
+        host = torch.empty(ncore, dtype=torch.int64, pin_memory=True)
+        host.copy_(bufs["levels"][:ncore], non_blocking=True)  # same stream: ordered before the next solve
+        pending.append((host, _trace_from_c(tr), step, rel))
+    comp.synchronize()
+    return [StackResult(None, trace, np.reshape(host.numpy(), ranks, order="F"), step, rel)
+            for host, trace, step, rel in pending]
 
 
 # ---------------------------------------------------------------------------

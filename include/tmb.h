@@ -102,6 +102,18 @@ int tmb_color_f64(tmb_ctx* ctx, const double* px_dev, int64_t npx, int space, do
 int tmb_color_inv_f64(tmb_ctx* ctx, const double* px_dev, int64_t npx, int space,
                       double* out_dev, int64_t* n_clamped_host);
 
+/* The latent codec's float64 colour path: n_img interleaved float64 RGB images
+ * (n_img, h, w, 3) -- the scene's ColorImage.pixels in (view, exposure) order --
+ * through to_coding_space (color.py:185-194, codec.py:389) straight into the
+ * per-channel layout of stack_to_tensor (sceneio.py:191-199): three float64
+ * F-order (h, w, E, V) tensors back to back (channel c at out + c*h*w*n_img).
+ * tmb_channels_to_rgb is the decode side's inverse (tensor_to_stack,
+ * sceneio.py:202-226, then to_rgb per image, codec.py:466-468). */
+int tmb_color_f64_channels(tmb_ctx* ctx, const double* px_dev, int64_t n_img, int64_t h, int64_t w, int space,
+                           double* tensor_dev);
+int tmb_channels_to_rgb(tmb_ctx* ctx, const double* tensor_dev, int64_t n_img, int64_t h, int64_t w, int space,
+                        double* rgb_out_dev);
+
 /* Decode side: tensor_dev is a reconstructed coding-space
  * stack (float64 F-order h x w x 3 x n_img: reconstruct(dequantize(q)),
  * codec.py:446-447); every pixel goes through to_rgb (color.py:197-205).
@@ -163,6 +175,15 @@ int tmb_tucker_als(tmb_ctx* ctx, const void* x_dev, int dtype, int order, const 
                    const int64_t* ranks, const tmb_solve_cfg* cfg, double* core_dev,
                    double* const* factors_dev, tmb_trace* trace);
 
+/* _solve_channels (codec.py:366-374): the latent path's three per-channel
+ * tucker_als solves in one call. x_dev holds the three (dims) tensors back to
+ * back (channel c at x_dev + c*prod(dims) elements of dtype); cores_dev[c],
+ * factors_dev[4c + n] and traces[c] (each may be NULL) receive channel c's
+ * model and trace. Same validation and error text as tmb_tucker_als. */
+int tmb_solve_channels(tmb_ctx* ctx, const void* x_dev, int dtype, const int64_t* dims, const int64_t* ranks,
+                       const tmb_solve_cfg* cfg, double* const* cores_dev, double* const* factors_dev,
+                       tmb_trace* traces);
+
 /* ---- codec (codec.py) --------------------------------------------------- */
 /* quantize_core (codec.py:114-134): int64 levels, step returned to host. */
 int tmb_quantize_core(tmb_ctx* ctx, const double* core_dev, int64_t n, int qp,
@@ -180,6 +201,16 @@ int tmb_varint_encode(tmb_ctx* ctx, const int64_t* levels_dev, int64_t n, uint8_
                       int64_t* nbytes_host);
 int tmb_varint_decode(tmb_ctx* ctx, const uint8_t* in_dev, int64_t nbytes, int64_t count, int64_t* levels_dev,
                       int64_t* used_host);
+
+/* Entropy stage tag 1 (entropy.py:37-52): the reference's adaptive order-0
+ * range coder (_kernels_py.py:24-109, _kernels.pyx:27-141), byte-identical, on
+ * HOST buffers (serial byte work after the device path; no context needed).
+ * tmb_rc_bound gives an output capacity sufficient for n input bytes; encode
+ * returns the byte count in *n_out (EINVAL if cap is too small); decode reads
+ * exactly n symbols (missing input bytes read as 0, as in the reference). */
+int tmb_rc_bound(int64_t n, int64_t* cap);
+int tmb_rc_encode(const uint8_t* in, int64_t n, uint8_t* out, int64_t cap, int64_t* n_out);
+int tmb_rc_decode(const uint8_t* in, int64_t n_in, int64_t n, uint8_t* out);
 
 /* ---- fused hot path ------------------------------------------------------
  * One stack end to end: u8 images -> colour (tmb_color_u8) -> tucker_als ->

@@ -76,6 +76,12 @@ SIGNATURES = {
     "tmb_tucker_als": ([_vp, _vp, _int, _int, _pi64, _pi64, C.POINTER(SolveCfg), _vp, _pvp, C.POINTER(Trace)], _int),
     "tmb_quantize_core": ([_vp, _vp, _i64, _int, _vp, C.POINTER(_dbl)], _int),
     "tmb_dequantize": ([_vp, _vp, _i64, _dbl, _vp], _int),
+    "tmb_color_f64_channels": ([_vp, _vp, _i64, _i64, _i64, _int, _vp], _int),
+    "tmb_channels_to_rgb": ([_vp, _vp, _i64, _i64, _i64, _int, _vp], _int),
+    "tmb_solve_channels": ([_vp, _vp, _int, _pi64, _pi64, C.POINTER(SolveCfg), _pvp, _pvp, C.POINTER(Trace)], _int),
+    "tmb_rc_bound": ([_i64, _pi64], _int),
+    "tmb_rc_encode": ([_vp, _i64, _vp, _i64, _pi64], _int),
+    "tmb_rc_decode": ([_vp, _i64, _i64, _vp], _int),
     "tmb_encode_stack_u8": ([_vp, _vp, _i64, _i64, _i64, _int, _pi64, C.POINTER(SolveCfg), _int, _vp, _vp, _pvp,
                              _vp, C.POINTER(_dbl), C.POINTER(Trace), C.POINTER(_dbl)], _int),
 }

@@ -18,15 +18,26 @@ template <typename F>
 int guard(tmb_ctx* ctx, F&& f) {
   if (!ctx) return TMB_EINVAL;
   ctx->c.err.clear();
+  // workspace mark: a throwing call skips its frames' arena releases, so the
+  // guard rewinds the arena to where the call started (after the stream has
+  // drained any work that may still use it)
+  const size_t mk = ctx->c.arena.mark();
+  auto rewind = [&]() {
+    cudaStreamSynchronize(ctx->c.stream);
+    cudaGetLastError();
+    ctx->c.arena.release(mk);
+  };
   try {
     TMB_CUDA(cudaSetDevice(ctx->c.device));
     f(ctx->c);
     return TMB_OK;
   } catch (const Error& e) {
     ctx->c.err = e.what();
+    rewind();
     return e.code;
   } catch (const std::exception& e) {
     ctx->c.err = e.what();
+    rewind();
     return TMB_ECUDA;
   }
 }
@@ -304,6 +315,46 @@ int tmb_tucker_als(tmb_ctx* ctx, const void* x, int dtype, int order, const int6
     if (cfg->max_sweeps < 0) throw Error(TMB_EINVAL, "max_sweeps must be >= 0");
     if (trace && trace->capacity < cfg->max_sweeps + 1) throw Error(TMB_EINVAL, "trace capacity < max_sweeps + 1");
     tmb::tucker_als_dev(c, x, to_dtype(dtype), d, r, *cfg, core, factors, trace);
+  });
+}
+
+int tmb_solve_channels(tmb_ctx* ctx, const void* x, int dtype, const int64_t* dims, const int64_t* ranks,
+                       const tmb_solve_cfg* cfg, double* const* cores, double* const* factors, tmb_trace* traces) {
+  return guard(ctx, [&](tmb::Ctx& c) {
+    const Dims d = to_dims(4, dims);
+    if (!cfg) throw Error(TMB_EINVAL, "null solve config");
+    const Dims r = check_ranks(d, ranks);
+    if (cfg->fit_tol <= 0 || cfg->pp_exit_tol <= 0) throw Error(TMB_EINVAL, "tolerances must be positive");
+    if (cfg->max_sweeps < 0) throw Error(TMB_EINVAL, "max_sweeps must be >= 0");
+    if (!cores || !factors) throw Error(TMB_EINVAL, "null output arrays");
+    for (int ch = 0; ch < 3; ++ch)
+      if (traces && traces[ch].capacity < cfg->max_sweeps + 1)
+        throw Error(TMB_EINVAL, "trace capacity < max_sweeps + 1");
+    const tmb::DType t = to_dtype(dtype);
+    const int64_t P = tmb::prod(d, 0, 4);
+    const size_t esz = t == tmb::F32 ? sizeof(float) : sizeof(double);
+    for (int ch = 0; ch < 3; ++ch) {
+      const void* xc = static_cast<const char*>(x) + (size_t)ch * (size_t)P * esz;
+      tmb::tucker_als_dev(c, xc, t, d, r, *cfg, cores[ch], factors + 4 * ch, traces ? traces + ch : nullptr);
+    }
+  });
+}
+
+int tmb_color_f64_channels(tmb_ctx* ctx, const double* px, int64_t n_img, int64_t h, int64_t w, int space,
+                           double* out) {
+  return guard(ctx, [&](tmb::Ctx& c) {
+    if (space < TMB_SPACE_RGB || space > TMB_SPACE_IPT) throw Error(TMB_EINVAL, "unknown color space");
+    if (n_img < 0 || h < 0 || w < 0) throw Error(TMB_EINVAL, "negative image dimensions");
+    tmb::color_f64_channels(c, px, n_img, h, w, space, out);
+  });
+}
+
+int tmb_channels_to_rgb(tmb_ctx* ctx, const double* t, int64_t n_img, int64_t h, int64_t w, int space,
+                        double* rgb) {
+  return guard(ctx, [&](tmb::Ctx& c) {
+    if (space < TMB_SPACE_RGB || space > TMB_SPACE_IPT) throw Error(TMB_EINVAL, "unknown color space");
+    if (n_img < 0 || h < 0 || w < 0) throw Error(TMB_EINVAL, "negative image dimensions");
+    tmb::channels_to_rgb(c, t, n_img, h, w, space, rgb);
   });
 }
 

@@ -274,6 +274,69 @@ __global__ void k_color_inv(const double* __restrict__ px, int64_t npx, int spac
   }
 }
 
+// The codec's float64 path (codec.py:389 then stack_to_tensor, sceneio.py:191-199):
+// n_img interleaved float64 images (img, h, w, 3) -- ColorImage.pixels of the
+// scene in (view, exposure) order -- through to_coding_space into three float64
+// F-order (h, w, E, V) channel tensors, plane (c n_img + img). 32 x 32 pixel
+// tiles transposed through shared memory: pixel reads along w, writes along h.
+__global__ void __launch_bounds__(256) k_color_f64_channels(const double* __restrict__ px, int64_t n_img,
+                                                            int64_t h, int64_t w, int space,
+                                                            double* __restrict__ out) {
+  __shared__ double so[3][32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t img = blockIdx.z, h0 = (int64_t)blockIdx.y * 32, w0 = (int64_t)blockIdx.x * 32;
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t hh = h0 + r, ww = w0 + tx;
+    if (hh < h && ww < w) {
+      const double* p = px + ((img * h + hh) * w + ww) * 3;
+      double o[3];
+      if (space == TMB_SPACE_YCBCR) {
+        ycbcr(p[0], p[1], p[2], o);
+      } else if (space == TMB_SPACE_IPT) {
+        const double lin[3] = {eotf(p[0]), eotf(p[1]), eotf(p[2])};
+        ipt_from_lin(lin, o);
+      } else {
+        o[0] = p[0]; o[1] = p[1]; o[2] = p[2];
+      }
+      for (int c = 0; c < 3; ++c) so[c][tx][r] = o[c];
+    }
+  }
+  __syncthreads();
+  const int64_t plane = h * w;
+  for (int col = ty; col < 32; col += 8) {
+    const int64_t hh = h0 + tx, ww = w0 + col;
+    if (hh < h && ww < w)
+      for (int c = 0; c < 3; ++c) out[(c * n_img + img) * plane + ww * h + hh] = so[c][col][tx];
+  }
+}
+
+// decode_stream's last steps (codec.py:446-468): three float64 (h, w, E, V)
+// channel tensors (reconstruct(dequantize(q)) per channel) -> tensor_to_stack
+// -> to_rgb per image, written as interleaved float64 RGB images (img, h, w, 3).
+__global__ void __launch_bounds__(256) k_channels_to_rgb(const double* __restrict__ t, int64_t n_img, int64_t h,
+                                                         int64_t w, int space, double* __restrict__ rgb) {
+  __shared__ double si[3][32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t img = blockIdx.z, h0 = (int64_t)blockIdx.y * 32, w0 = (int64_t)blockIdx.x * 32;
+  const int64_t plane = h * w;
+  for (int col = ty; col < 32; col += 8) {
+    const int64_t hh = h0 + tx, ww = w0 + col;
+    if (hh < h && ww < w)
+      for (int c = 0; c < 3; ++c) si[c][col][tx] = t[(c * n_img + img) * plane + ww * h + hh];
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t hh = h0 + r, ww = w0 + tx;
+    if (hh < h && ww < w) {
+      double o[3];
+      int cl;
+      inv_px(space, si[0][tx][r], si[1][tx][r], si[2][tx][r], o, &cl);
+      double* q = rgb + ((img * h + hh) * w + ww) * 3;
+      q[0] = o[0]; q[1] = o[1]; q[2] = o[2];
+    }
+  }
+}
+
 // Decode side: the reconstructed coding-space stack
 // (F-order h x w x 3 x n_img fp64, reconstruct(dequantize(q)), codec.py:446-447)
 // -> to_rgb per pixel (color.py:197-205) -> optional interleaved RGB output and
@@ -442,6 +505,24 @@ void color_inv_f64(Ctx& c, const double* px, int64_t npx, int space, double* out
   TMB_CUDA(cudaStreamSynchronize(c.stream));
   if (n_clamped) *n_clamped = (int64_t)hc;
   c.arena.release(mk);
+}
+
+void color_f64_channels(Ctx& c, const double* px, int64_t n_img, int64_t h, int64_t w, int space, double* out) {
+  if (n_img == 0 || h == 0 || w == 0) return;
+  ensure_constants(c);
+  dim3 grid((unsigned)ceil_div(w, 32), (unsigned)ceil_div(h, 32), (unsigned)n_img);
+  k_color_f64_channels<<<grid, dim3(32, 8), 0, c.stream>>>(px, n_img, h, w, space, out);
+  c.launches++;
+  check_launch("k_color_f64_channels");
+}
+
+void channels_to_rgb(Ctx& c, const double* t, int64_t n_img, int64_t h, int64_t w, int space, double* rgb) {
+  if (n_img == 0 || h == 0 || w == 0) return;
+  ensure_constants(c);
+  dim3 grid((unsigned)ceil_div(w, 32), (unsigned)ceil_div(h, 32), (unsigned)n_img);
+  k_channels_to_rgb<<<grid, dim3(32, 8), 0, c.stream>>>(t, n_img, h, w, space, rgb);
+  c.launches++;
+  check_launch("k_channels_to_rgb");
 }
 
 void decode_sse(Ctx& c, const double* t, int64_t n_img, int64_t h, int64_t w, int space, const uint8_t* rgb,

@@ -158,6 +158,10 @@ void color_u8(Ctx& c, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, i
               bool channel_major = false);
 void color_f64(Ctx& c, const double* rgb, int64_t npx, int space, double* out);
 void color_inv_f64(Ctx& c, const double* px, int64_t npx, int space, double* out, int64_t* n_clamped);
+// codec float64 path: interleaved (img, h, w, 3) pixels -> three F-order (h, w, E, V) channel tensors
+void color_f64_channels(Ctx& c, const double* px, int64_t n_img, int64_t h, int64_t w, int space, double* out);
+// inverse: three (h, w, E, V) channel tensors -> to_rgb -> interleaved (img, h, w, 3)
+void channels_to_rgb(Ctx& c, const double* t, int64_t n_img, int64_t h, int64_t w, int space, double* rgb);
 // decode: coding-space F-order stack -> RGB (optional interleaved output) and the
 // per-image SSE in 8-bit units vs the original u8 images (rgb may be null)
 void decode_sse(Ctx& c, const double* t, int64_t n_img, int64_t h, int64_t w, int space, const uint8_t* rgb,

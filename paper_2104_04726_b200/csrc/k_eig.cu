@@ -902,7 +902,6 @@ __global__ void k_larft(const double* __restrict__ S, const double* __restrict__
   for (int e = r; e < nb * nb; e += blockDim.x) T[(int64_t)p * nb * nb + e] = sT[e];
 }
 
-struct CoopInfo { int blocks = 0; int64_t n = -1; };
 
 }  // namespace
 
@@ -1310,12 +1309,7 @@ static void backtransform(Ctx& c, const double* hv, const double* tau, int64_t n
     g.C = S; g.sCm = 1; g.sCn = nb; g.sCb = nb * nb;
     gemm(c, g);
   }
-  static bool larft_attr = false;
-  if (!larft_attr) {
-    TMB_CUDA(cudaFuncSetAttribute(k_larft, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double) * (2 * 64 * 64 + 64))));
-    larft_attr = true;
-  }
+  set_smem_attr(c, (const void*)k_larft, sizeof(double) * (2 * 64 * 64 + 64));
   k_larft<<<np, nb, sizeof(double) * (2 * nb * nb + nb), c.stream>>>(S, tau, nb, T);
   LAUNCHED("k_larft");
   // (A fused one-kernel variant that streams every panel through shared memory
@@ -1350,12 +1344,7 @@ static void backtransform(Ctx& c, const double* hv, const double* tau, int64_t n
     if (pick) {
       const void* fn = pick == 2 ? (const void*)k_apply_wy_cl<2, 2>
                      : pick == 4 ? (const void*)k_apply_wy_cl<4, 2> : (const void*)k_apply_wy_cl<8, 2>;
-      static bool attr[3] = {false, false, false};
-      const int ai = pick == 2 ? 0 : (pick == 4 ? 1 : 2);
-      if (!attr[ai]) {
-        TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr[ai] = true;
-      }
+      set_smem_attr(c, fn, 227 * 1024);
       Timed timed(c, TAG_EIG_GEMM, 4.0 * (double)n * n * k / 2);
       cudaLaunchConfig_t lc{};
       lc.gridDim = dim3((unsigned)(groups * pick));
@@ -1383,11 +1372,7 @@ static void backtransform(Ctx& c, const double* hv, const double* tau, int64_t n
       sizeof(double) * ((size_t)ST * wy::NB * (RC + 4) + (size_t)CB * ldx + 8 * wy::LDW + 4 * 32 * 4);
   static const bool fused_off = std::getenv("TMB_WY_GEMMS") != nullptr;  // A/B: per-panel GEMM path
   if (!fused_off && nb == wy::NB && fsmem <= 227 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      TMB_CUDA(cudaFuncSetAttribute(k_apply_wy<CB, RC, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      attr = true;
-    }
+    set_smem_attr(c, (const void*)k_apply_wy<CB, RC, ST>, 227 * 1024);
     const int vec = (n % 2 == 0 && reinterpret_cast<uintptr_t>(hv) % 16 == 0 &&
                      reinterpret_cast<uintptr_t>(VT) % 16 == 0) ? 1 : 0;
     Timed timed(c, TAG_EIG_GEMM, 4.0 * (double)n * n * k / 2);
@@ -1427,12 +1412,7 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
   if (n <= 0 || k <= 0) return;
   if (n <= JAC_MAX) {
     const size_t smem = sizeof(double) * 2 * n * (n + 1);
-    static bool attr = false;
-    if (!attr) {
-      TMB_CUDA(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)(sizeof(double) * 2 * JAC_MAX * (JAC_MAX + 1))));
-      attr = true;
-    }
+    set_smem_attr(c, (const void*)k_jacobi, sizeof(double) * 2 * JAC_MAX * (JAC_MAX + 1));
     k_jacobi<<<1, 256, smem, c.stream>>>(g, (int)n, (int)k, vecs, vals);
     LAUNCHED("k_jacobi");
     return;
@@ -1452,20 +1432,13 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
   copy_d(c, A, g, n * n);
   // cooperative grid sized to co-residency
   const size_t smem = sizeof(double) * (3 * n + 48);
-  static CoopInfo info;
-  if (info.n != n) {
-    TMB_CUDA(cudaFuncSetAttribute(k_sytrd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)std::max<size_t>(smem, 48 * 1024)));
-    int per_sm = 0;
-    TMB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sytrd, TRD_THREADS, smem));
-    if (per_sm < 1) throw Error(TMB_EINVAL, "leading_eigvecs: matrix too large for the cooperative reduction");
-    // one trailing column per warp when possible
-    info.blocks = (int)std::min<int64_t>((int64_t)per_sm * c.num_sms,
-                                         std::max<int64_t>(1, ceil_div(n, TRD_THREADS / 32)));
-    info.n = n;
-  }
+  set_smem_attr(c, (const void*)k_sytrd, std::max<size_t>(smem, 48 * 1024));
+  const int per_sm = blocks_per_sm(c, (const void*)k_sytrd, TRD_THREADS, smem);
+  if (per_sm < 1) throw Error(TMB_EINVAL, "leading_eigvecs: matrix too large for the cooperative reduction");
+  // one trailing column per warp when possible
+  const int blocks = (int)std::min<int64_t>((int64_t)per_sm * c.num_sms,
+                                            std::max<int64_t>(1, ceil_div(n, TRD_THREADS / 32)));
   const void* kern = (const void*)k_sytrd;
-  const int blocks = info.blocks;
   double* part = alloc<double>(c, 2 * (size_t)blocks);
   // Steps 0..K0-1 grid-wide; the trailing (n-K0-1)-block goes to the cluster
   // kernel (one cluster barrier per column instead of a grid barrier).
@@ -1540,11 +1513,7 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
     static const bool tw_global = std::getenv("TMB_TWISTED_GLOBAL") != nullptr;  // A/B: L2 scratch variant
     const size_t tw_smem = sizeof(double) * 2 * (size_t)n;  // per eigenvalue
     if (!tw_global && tw_smem <= 200 * 1024) {
-      static bool tw_attr = false;
-      if (!tw_attr) {
-        TMB_CUDA(cudaFuncSetAttribute(k_twisted_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        tw_attr = true;
-      }
+      set_smem_attr(c, (const void*)k_twisted_sm, 200 * 1024);
       k_twisted_sm<<<(unsigned)k, 64, tw_smem, c.stream>>>(d, e, n, k, vals, vecs);
       LAUNCHED("k_twisted_sm");
     } else {

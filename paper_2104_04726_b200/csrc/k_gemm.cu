@@ -258,12 +258,7 @@ __global__ void k_mirror(double* g, int64_t n, int batch, int64_t sb) {
 template <typename TA, typename TB, bool AMF, bool BNF>
 void launch_t(Ctx& c, const KArgs& a, dim3 grid) {
   const size_t smem = (size_t)ST * (Tile<TA, AMF, BM>::SIZE * sizeof(TA) + Tile<TB, BNF, BN>::SIZE * sizeof(TB));
-  static bool attr = false;
-  if (!attr) {
-    TMB_CUDA(cudaFuncSetAttribute(k_gemm_dmma<TA, TB, AMF, BNF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    attr = true;
-  }
+  set_smem_attr(c, (const void*)k_gemm_dmma<TA, TB, AMF, BNF>, smem);
   k_gemm_dmma<TA, TB, AMF, BNF><<<grid, NT, smem, c.stream>>>(a);
   c.launches++;
   check_launch("k_gemm_dmma");

@@ -746,11 +746,7 @@ void ozaki_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t R,
     const CUtensorMap ta4 = digit_map(su, Up, Kp, OZ_BM, 4), tb7 = digit_map(sx, Xp, Kp, OZ2_BN, 7),
                       tb4 = digit_map(sx, Xp, Kp, OZ2_BN, 4);
     const size_t smem = (size_t)OZ2_ST * OZ2_STAGE + 1024;
-    static bool attr2 = false;
-    if (!attr2) {
-      TMB_CUDA(cudaFuncSetAttribute(k_oz_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr2 = true;
-    }
+    set_smem_attr(c, (const void*)k_oz_gemm2, smem);
     k_oz_gemm2<<<grid, OZ2_NT, smem, c.stream>>>(ta4, tb7, tb4, eu, ex, L, R, N, Kp, y);
     c.launches++;
     check_launch("k_oz_gemm2");
@@ -765,11 +761,7 @@ void ozaki_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t R,
                       tb = digit_map(sx, Xp, Kp, (uint32_t)bn, OZ_S, (uint32_t)bkb);
     const size_t smem = (bkb == 64 ? 2 : 4) * (size_t)OZ_S * (OZ_BM + OZ_BN) * bkb + 1024;
     const void* fn = bkb == 64 ? (const void*)k_oz_gemm<64> : (const void*)k_oz_gemm<32>;
-    static bool attr[2] = {false, false};
-    if (!attr[bkb == 64]) {
-      TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr[bkb == 64] = true;
-    }
+    set_smem_attr(c, fn, smem);
     if (bkb == 64) k_oz_gemm<64><<<grid, OZ_NT, smem, c.stream>>>(ta, tb, eu, ex, L, R, N, Kp, y);
     else k_oz_gemm<32><<<grid, OZ_NT, smem, c.stream>>>(ta, tb, eu, ex, L, R, N, Kp, y);
     c.launches++;

@@ -408,13 +408,9 @@ bool small_ttm2(Ctx& c, const void* x, DType tx, int64_t L, int64_t K1, int64_t 
   if (total == 0) return true;
   const size_t smem = sizeof(double) * (K1 * r1 + K2 * r2 + (size_t)K2 * r1 * ST2_THREADS);
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, ST2_THREADS), 32LL * c.num_sms));
-  static bool attr[2] = {false, false};  // > 48 KB of per-thread inner sums (e.g. view-exposure 18 -> 9)
-  if (!attr[tx == F32 ? 0 : 1]) {
-    const void* fn = tx == F32 ? (const void*)k_small_ttm2<float> : (const void*)k_small_ttm2<double>;
-    TMB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double) * (64 * 8 + 64 * 64 + (size_t)ST2_T * ST2_THREADS))));
-    attr[tx == F32 ? 0 : 1] = true;
-  }
+  // > 48 KB of per-thread inner sums (e.g. view-exposure 18 -> 9)
+  set_smem_attr(c, tx == F32 ? (const void*)k_small_ttm2<float> : (const void*)k_small_ttm2<double>,
+                sizeof(double) * (64 * 8 + 64 * 64 + (size_t)ST2_T * ST2_THREADS));
   if (tx == F32)
     k_small_ttm2<float><<<blocks, ST2_THREADS, smem, c.stream>>>((const float*)x, L, (int)K1, (int)K2, Rr, m1,
                                                                   (int)r1, s1r, s1k, m2, (int)r2, s2r, s2k, y);

@@ -584,7 +584,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
   }
 }
 
-struct RowsInfo { int blocks = 0; int64_t n = -1; };
 
 }  // namespace
 
@@ -610,32 +609,24 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
   static const bool rpt4_env = std::getenv("TMB_SMEM_RPT4") != nullptr;  // A/B: 4 rows/thread for n <= 1536
   using KFn = void (*)(RowArgs, int, long long*);
   KFn kern = nullptr;
-  int slot = 0;
   const int qmax = (int)ceil_div(n - 1, nb);
   static const bool prof_on = std::getenv("TMB_TRD_PROFILE") != nullptr;
 #define SMEM_K(R, T) (prof_on ? k_sytrd_smem<R, T, true> : k_sytrd_smem<R, T, false>)
   if (nt == 512) {
-    if (rpt <= 2) { kern = SMEM_K(2, 512); slot = 0; }
-    else if (rpt <= 3 && !rpt4_env) { kern = SMEM_K(3, 512); slot = 4; }  // n <= 1536 (C2 mode 0)
-    else if (rpt <= 4) { kern = SMEM_K(4, 512); slot = 1; }
+    if (rpt <= 2) { kern = SMEM_K(2, 512); }
+    else if (rpt <= 3 && !rpt4_env) { kern = SMEM_K(3, 512); }  // n <= 1536 (C2 mode 0)
+    else if (rpt <= 4) { kern = SMEM_K(4, 512); }
   } else {
-    if (rpt <= 4) { kern = SMEM_K(4, 256); slot = 2; }
-    else if (rpt <= 8) { kern = SMEM_K(8, 256); slot = 3; }
+    if (rpt <= 4) { kern = SMEM_K(4, 256); }
+    else if (rpt <= 8) { kern = SMEM_K(8, 256); }
   }
 #undef SMEM_K
   if (!kern) return false;
   const int nw = nt / 32;
   const size_t smem = sizeof(double) * (((size_t)qmax * n + 1) / 2 * 2 + (size_t)nw * qmax + 2 * nw + 2 * qmax + 1);
   if (smem > 227 * 1024) return false;
-  static int64_t checked[5] = {-1, -1, -1, -1, -1};
-  if (checked[slot] != n) {
-    TMB_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)std::max<size_t>(smem, 48 * 1024)));
-    int per_sm = 0;
-    TMB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kern, nt, smem));
-    if (per_sm < bps) return false;
-    checked[slot] = n;
-  }
+  set_smem_attr(c, (const void*)kern, std::max<size_t>(smem, 48 * 1024));
+  if (blocks_per_sm(c, (const void*)kern, nt, smem) < bps) return false;
   // TMB_TRD_PROFILE: per-phase clock64 sums (blocks 0 and NB/2, by quarter of the reduction)
   long long* prof = nullptr;
   if (prof_on) {
@@ -683,42 +674,35 @@ bool sytrd_rows(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
   }();
   using KFn = void (*)(RowArgs);
   KFn kern;
-  int slot, nt;
+  int nt;
   // measured (scripts/ab_rows.sh): 512 threads win only for large n (n=1920:
   // 15.2 vs 16.2 ms; n=1080: 7.3 vs 6.9 ms)
   const bool big_blocks = nt_env == 512 || (nt_env == 0 && n > 1536);
   if (big_blocks) {
     nt = 512;
     const int rpt = (int)ceil_div(n, 512);
-    if (rpt <= 2) { kern = cb_env == 1 ? k_sytrd_rows<2, 1, 512> : k_sytrd_rows<2, 2, 512>; slot = 4; }
-    else { kern = cb_env == 1 ? k_sytrd_rows<4, 1, 512> : k_sytrd_rows<4, 2, 512>; slot = 5; }
+    if (rpt <= 2) { kern = cb_env == 1 ? k_sytrd_rows<2, 1, 512> : k_sytrd_rows<2, 2, 512>; }
+    else { kern = cb_env == 1 ? k_sytrd_rows<4, 1, 512> : k_sytrd_rows<4, 2, 512>; }
   } else {
     nt = 256;
     const int rpt = (int)ceil_div(n, 256);
     // defaults from scripts/ab_rows.sh: CB 2 / 2 / 1 / 2 for RPT 2 / 4 / 6 / 8
-    if (rpt <= 2) { kern = cb_env == 1 ? k_sytrd_rows<2, 1, 256> : k_sytrd_rows<2, 2, 256>; slot = 0; }
-    else if (rpt <= 4) { kern = cb_env == 1 ? k_sytrd_rows<4, 1, 256> : k_sytrd_rows<4, 2, 256>; slot = 1; }
-    else if (rpt <= 6) { kern = cb_env == 2 ? k_sytrd_rows<6, 2, 256> : k_sytrd_rows<6, 1, 256>; slot = 2; }
-    else { kern = cb_env == 1 ? k_sytrd_rows<8, 1, 256> : k_sytrd_rows<8, 2, 256>; slot = 3; }
+    if (rpt <= 2) { kern = cb_env == 1 ? k_sytrd_rows<2, 1, 256> : k_sytrd_rows<2, 2, 256>; }
+    else if (rpt <= 4) { kern = cb_env == 1 ? k_sytrd_rows<4, 1, 256> : k_sytrd_rows<4, 2, 256>; }
+    else if (rpt <= 6) { kern = cb_env == 2 ? k_sytrd_rows<6, 2, 256> : k_sytrd_rows<6, 1, 256>; }
+    else { kern = cb_env == 1 ? k_sytrd_rows<8, 1, 256> : k_sytrd_rows<8, 2, 256>; }
   }
   const size_t smem = sizeof(double) * (2 * n + (nt / 32) * 64 + 2 * (nt / 32));
-  static RowsInfo info[6];
-  if (info[slot].n != n) {
-    TMB_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)std::max<size_t>(smem, 48 * 1024)));
-    int per_sm = 0;
-    TMB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kern, nt, smem));
-    if (per_sm < 1) return false;
-    // at most 64 owned columns per block (the partial array), ~n/NB per block
-    const int64_t need = ceil_div(n, 64);
-    int64_t blocks = std::min<int64_t>((int64_t)per_sm * c.num_sms, std::max<int64_t>(n, 1));
-    if (blocks < need) return false;
-    info[slot].blocks = (int)blocks;
-    info[slot].n = n;
-  }
+  set_smem_attr(c, (const void*)kern, std::max<size_t>(smem, 48 * 1024));
+  const int per_sm = blocks_per_sm(c, (const void*)kern, nt, smem);
+  if (per_sm < 1) return false;
+  // at most 64 owned columns per block (the partial array), ~n/NB per block
+  const int64_t need = ceil_div(n, 64);
+  const int64_t blocks = std::min<int64_t>((int64_t)per_sm * c.num_sms, std::max<int64_t>(n, 1));
+  if (blocks < need) return false;
   RowArgs ra{A, n, k_end, d, e, tau, hv, pbuf};
   void* args[] = {&ra};
-  TMB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, info[slot].blocks, nt, args, smem, c.stream));
+  TMB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, (int)blocks, nt, args, smem, c.stream));
   c.launches++;
   check_launch("k_sytrd_rows");
   return true;

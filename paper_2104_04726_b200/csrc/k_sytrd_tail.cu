@@ -11,6 +11,9 @@
 // scratch (K0 = 0), so small matrices never touch the grid kernel.
 #include <cooperative_groups.h>
 
+#include <map>
+#include <mutex>
+
 #include "tmb_internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -225,11 +228,8 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_sytrd_tail(const TailArgs a
 
 struct TailCfg { int cl = 0; int64_t max_m = 0; const void* fn = nullptr; };
 
-TailCfg tail_config(Ctx& c) {
-  static TailCfg cfg;
-  static bool init = false;
-  if (init) return cfg;
-  init = true;
+TailCfg tail_config_compute(Ctx& c) {
+  TailCfg cfg;
   int smem_optin = 0;
   TMB_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
   for (int cl : {16, 8}) {
@@ -263,6 +263,18 @@ TailCfg tail_config(Ctx& c) {
     }
     cudaGetLastError();
   }
+  return cfg;
+}
+
+// per device (cluster attributes and occupancy are per device context), thread-safe
+TailCfg tail_config(Ctx& c) {
+  static std::mutex mu;
+  static std::map<int, TailCfg> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(c.device);
+  if (it != cache.end()) return it->second;
+  const TailCfg cfg = tail_config_compute(c);
+  cache[c.device] = cfg;
   return cfg;
 }
 

@@ -195,12 +195,7 @@ void sytrd_tail1(Ctx& c, double* A, int64_t n, int64_t K0, double* d, double* e,
   const int64_t m = n - K0 - 1;
   if (m < 2 || m > T1_MAX) throw Error(TMB_EINVAL, "sytrd_tail1: trailing block size out of range");
   const size_t smem = sizeof(double) * ((size_t)m * m + (3 + T1_PARTS) * (size_t)m + 2);
-  static bool attr = false;
-  if (!attr) {
-    TMB_CUDA(cudaFuncSetAttribute((const void*)k_sytrd_tail1, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double) * (T1_MAX * T1_MAX + (3 + T1_PARTS) * T1_MAX + 2))));
-    attr = true;
-  }
+  set_smem_attr(c, (const void*)k_sytrd_tail1, sizeof(double) * (T1_MAX * T1_MAX + (3 + T1_PARTS) * T1_MAX + 2));
   static const bool prof_on = std::getenv("TMB_TRD_PROFILE") != nullptr;
   long long* prof = nullptr;
   if (prof_on) {

@@ -96,6 +96,12 @@ T* alloc(Ctx& c, size_t n) { return static_cast<T*>(c.arena.alloc(n * sizeof(T))
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Per-(device, kernel) attribute / occupancy caches (devcache.cu): raise the
+// kernel's dynamic shared-memory limit to at least `bytes` on c.device once;
+// resident blocks per SM for (kernel, threads, smem) on c.device.
+void set_smem_attr(Ctx& c, const void* fn, size_t bytes);
+int blocks_per_sm(Ctx& c, const void* fn, int threads, size_t smem);
+
 // ---------------------------------------------------------------- GEMM (k_gemm.cu)
 enum DType { F32 = 0, F64 = 1 };
 

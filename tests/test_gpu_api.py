@@ -156,6 +156,31 @@ def test_eig_kernel_paths_vs_lapack(n, k):
     assert np.array_equal(v, v2) and np.array_equal(w, w2)  # deterministic
 
 
+@pytest.mark.parametrize("n,k", [(2160, 270), (3840, 480), (4320, 540), (7680, 960)])
+def test_eig_large_n_vs_lapack(n, k):
+    """The Gram sizes of BASELINE configs 4 and 5 (n = 2160, 3840, 4320, 7680;
+    k = the configs' ranks): column-kernel tridiagonalisation and the unfused
+    back-transform, against LAPACK (numpy eigh, the reference's dsyevd) and
+    the known spectral decomposition the matrix was built from."""
+    rng = np.random.default_rng(n + k)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = 1e3 * np.exp(-np.linspace(0, 18, n))
+    g = (q * lam) @ q.T
+    g = 0.5 * (g + g.T)
+    v, w = tb.leading_eigvecs(g, k)
+    vr, wr = oracle.leading_eigvecs(g, k)
+    from conftest import principal_angle
+
+    assert np.abs(v.T @ v - np.eye(k)).max() < 1e-12
+    assert np.abs(w - wr).max() / wr[0] < 1e-13
+    assert np.abs(w - lam[:k]).max() / lam[0] < 1e-13
+    assert np.abs(g @ v - v * w).max() / wr[0] < 1e-12
+    assert principal_angle(v, vr) < 1e-8
+    assert principal_angle(v, q[:, :k]) < 1e-8
+    # same sign rule as the reference: per-column agreement with LAPACK's sign-fixed vectors
+    assert np.abs(v - vr).max() < 1e-8
+
+
 def test_eig_deterministic():  # tests/test_tensor.py:218-223
     rng = np.random.default_rng(9)
     b = rng.standard_normal((300, 300))

@@ -1,0 +1,125 @@
+"""BASELINE configs 3, 4 and 5 at FULL size against the reference itself
+(compact goldens from scripts/make_golden_configs.py, SURVEY App. B bars):
+
+* c3  -- one full 10-sweep stack of the 64-frame batch, including App. B.1(ii):
+         the product chain from u8 (fp32 colour tensor) against the reference
+         chain from u8 (its own float64 colour tensor);
+* c4  -- the error-vs-rank curve at ranks 1/8, 1/4, 1/2 (T-HOSVD + 2 sweeps);
+* c5  -- the 8K stack, T-HOSVD + 2 sweeps (Grams of n = 4320 and 7680).
+
+Every check also pins App. B.6: trace length, `converged` and the index of the
+returned model.
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2104_04726_b200 as tb
+from paper_2104_04726_b200.synth import CONFIGS, make_stack
+
+pytestmark = pytest.mark.gpu
+
+
+def _best_index(fits) -> int:
+    b = 0
+    for i, f in enumerate(fits):
+        if f > fits[b]:
+            b = i
+    return b
+
+
+def _sketch(u: np.ndarray) -> np.ndarray:
+    w = np.random.default_rng(1000 + u.shape[0]).standard_normal((u.shape[0], 16)) / np.sqrt(u.shape[0])
+    p = w.T @ u
+    return p @ p.T
+
+
+def _check(res, z, tag: str, sketch_tol: float, fit_tol: float, rel_tol: float, head_tol: float) -> dict:
+    fits = np.array([r.fit for r in res.trace.records])
+    ref = z[f"{tag}trace_fit"]
+    # App. B.6: trace length, converged flag, returned-model index
+    assert len(fits) == len(ref)
+    assert bool(res.trace.converged) == bool(z[f"{tag}converged"])
+    assert _best_index(list(fits)) == int(z[f"{tag}best_index"])
+    assert [r.kind for r in res.trace.records] == list(z[f"{tag}trace_kind"])
+    out = {"fit": float(np.abs(fits - ref).max()), "rel": abs(res.rel_err - float(z[f"{tag}rel_err"]))}
+    assert out["fit"] < fit_tol, out
+    assert out["rel"] < rel_tol, out                      # north-star bar 1e-4
+    for n in range(4):
+        u = res.model.factors[n]
+        ds = float(np.abs(_sketch(u) - z[f"{tag}sketch{n}"]).max())
+        h = z[f"{tag}head{n}"]
+        dh = float(np.abs(u[:, : h.shape[1]] - h).max())
+        out[f"sketch{n}"], out[f"head{n}"] = ds, dh
+        assert ds < sketch_tol, (n, out)                  # subspace (bar 1e-3 rad)
+        assert dh < head_tol, (n, out)                    # leading eigenvectors, same sign rule
+    return out
+
+
+def _levels(res, z, tag: str, max_frac: float, step_rel: float = 1e-9) -> int:
+    assert float(res.step) == pytest.approx(float(z[f"{tag}step"]), rel=step_rel)
+    lv = res.levels.ravel(order="F").astype(np.int64)
+    if f"{tag}levels" in z:
+        ref = z[f"{tag}levels"].astype(np.int64)
+        mine = lv
+    else:
+        idx = z[f"{tag}levels_idx"]
+        ref = z[f"{tag}levels_sample"].astype(np.int64)
+        mine = lv[idx]
+    diff = mine != ref
+    nd = int(diff.sum())
+    # bit-exact except rounding ties: at most 1 LSB, on a vanishing fraction
+    assert (int(np.abs(mine - ref).max()) if nd else 0) <= 1
+    assert nd <= max_frac * ref.size, nd
+    return nd
+
+
+def _stack_and_sha(cfg, seed=0, frame=0):
+    images = make_stack(cfg, seed=seed, frame=frame)
+    t = tb.coding_tensor(images, cfg.space).cpu().numpy()
+    return images, hashlib.sha256(t.tobytes()).hexdigest()
+
+
+def test_c3_full_size_matches_reference(golden):
+    z = golden("c3_full")
+    cfg = CONFIGS["c3"]
+    images, sha = _stack_and_sha(cfg, int(z["seed"]), int(z["frame"]))
+    assert sha == str(z["tensor_f32_sha"])
+    res = tb.encode_stack(images, cfg.space, cfg.ranks, cfg.sweeps, cfg.qp)
+    _check(res, z, "", sketch_tol=1e-6, fit_tol=1e-9, rel_tol=1e-8, head_tol=1e-6)
+    _levels(res, z, "", 1e-5)
+    # App. B.1(ii): the reference solved its own float64 colour tensor; ours solved the
+    # fp32 tensor the colour kernel writes. Bars: angles 1e-3 rad, rel. error 1e-4,
+    # levels bit-exact except ties.
+    _check(res, z, "f64in_", sketch_tol=1e-3, fit_tol=1e-6, rel_tol=1e-4, head_tol=1e-3)
+    # the fp32 input moves max|core| (hence the step) by ~1e-9 relative
+    _levels(res, z, "f64in_", 1e-3, step_rel=1e-6)
+
+
+@pytest.mark.parametrize("name", ["c4_8", "c4_4", "c4_2"])
+def test_c4_error_vs_rank_curve_matches_reference(golden, name):
+    """BASELINE config 4: reconstruction error at ranks 1/8, 1/4, 1/2 of each
+    spatial mode (+ colour 3, exposure 7) against the reference, 2 sweeps."""
+    z = golden("c4_curve")
+    cfg = CONFIGS[name]
+    images, sha = _stack_and_sha(cfg, int(z["seed"]))
+    assert sha == str(z["tensor_f32_sha"])
+    assert tuple(z[f"{name}_ranks"]) == cfg.ranks
+    res = tb.encode_stack(images, cfg.space, cfg.ranks, int(z["sweeps"]), 51)
+    _check(res, z, f"{name}_", sketch_tol=1e-4, fit_tol=1e-9, rel_tol=1e-8, head_tol=1e-4)
+
+
+def test_c5_full_size_matches_reference(golden):
+    """BASELINE config 5 (4320x7680x3x18, ranks (540,960,3,9)) on one B200,
+    T-HOSVD + 2 sweeps, against the reference run (29 GB of host RAM)."""
+    z = golden("c5_2sweeps")
+    cfg = CONFIGS["c5"]
+    images, sha = _stack_and_sha(cfg, int(z["seed"]))
+    assert sha == str(z["tensor_f32_sha"])
+    res = tb.encode_stack(images, cfg.space, cfg.ranks, int(z["sweeps"]), cfg.qp)
+    _check(res, z, "", sketch_tol=1e-3, fit_tol=1e-9, rel_tol=1e-8, head_tol=1e-4)
+    _levels(res, z, "", 1e-2)

@@ -21,6 +21,7 @@
 
 #include <cfloat>
 #include <cstdlib>
+#include <functional>
 
 #include "tmb_internal.cuh"
 
@@ -902,42 +903,179 @@ __global__ void k_larft(const double* __restrict__ S, const double* __restrict__
   for (int e = r; e < nb * nb; e += blockDim.x) T[(int64_t)p * nb * nb + e] = sT[e];
 }
 
+// ------------------------------------------------------------------ cluster repair
+// Robust path for (near-)repeated eigenvalues (a rank-deficient Gram asked for
+// more vectors than its rank, e.g. hosvd of a (100, 3, 3) tensor: 91 zero
+// eigenvalues). The twisted factorisation computes each vector on its own, so
+// the members of a tight cluster come out (nearly) parallel. For every cluster
+// the tridiagonal vectors are replaced by an orthonormal basis of the
+// cluster's invariant subspace from block inverse iteration -- (T - sigma I)
+// Y = Y_prev with sigma inside the cluster, LU with partial pivoting (the
+// dgtsv elimination) and zero pivots perturbed to eps ||T||, then classical
+// Gram-Schmidt applied twice -- as LAPACK's dstein does with its
+// reorthogonalised inverse iteration.
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {  // splitmix64 finaliser
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__global__ void k_fill_rand(double* __restrict__ y, int64_t n, int64_t m, int64_t ldy, uint64_t seed) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * m; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % n, j = t / n;
+    const uint64_t h = mix64(seed ^ mix64((uint64_t)t));
+    y[j * ldy + i] = (double)(h >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+  }
+}
+
+// one thread per column: y_j <- (T - sigma I)^-1 y_j, T = tridiag(e, d, e);
+// scratch: 3 n doubles per column laid out [3][n][m] (coalesced across threads)
+__global__ void k_tri_shift_solve(const double* __restrict__ d, const double* __restrict__ e, int64_t n,
+                                  double sigma, double pert, double* __restrict__ y, int64_t ldy, int64_t m,
+                                  double* __restrict__ scr) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double* dl = scr;                 // sub-diagonal, becomes the 2nd super-diagonal after pivoting
+  double* dd = scr + n * m;         // diagonal
+  double* du = scr + 2 * n * m;     // super-diagonal
+  double* b = y + j * ldy;
+  auto at = [&](double* a, int64_t i) -> double& { return a[i * m + j]; };
+  for (int64_t i = 0; i < n; ++i) {
+    at(dd, i) = d[i] - sigma;
+    if (i + 1 < n) { at(dl, i) = e[i]; at(du, i) = e[i]; }
+  }
+  auto nz = [&](double v) { return v != 0.0 ? v : pert; };
+  for (int64_t i = 0; i + 1 < n; ++i) {
+    const double di = at(dd, i), li = at(dl, i);
+    if (fabs(di) >= fabs(li)) {  // no interchange
+      const double piv = nz(di);
+      at(dd, i) = piv;
+      const double f = li / piv;
+      at(dd, i + 1) -= f * at(du, i);
+      b[i + 1] -= f * b[i];
+      at(dl, i) = 0.0;
+    } else {                     // interchange rows i and i+1
+      const double f = di / li;
+      at(dd, i) = li;
+      const double t = at(dd, i + 1);
+      at(dd, i + 1) = at(du, i) - f * t;
+      if (i + 2 < n) {
+        at(dl, i) = at(du, i + 1);
+        at(du, i + 1) = -f * at(dl, i);
+      } else {
+        at(dl, i) = 0.0;
+      }
+      at(du, i) = t;
+      const double bt = b[i];
+      b[i] = b[i + 1];
+      b[i + 1] = bt - f * b[i + 1];
+    }
+  }
+  at(dd, n - 1) = nz(at(dd, n - 1));
+  b[n - 1] /= at(dd, n - 1);
+  if (n > 1) b[n - 2] = (b[n - 2] - at(du, n - 2) * b[n - 1]) / at(dd, n - 2);
+  for (int64_t i = n - 3; i >= 0; --i) b[i] = (b[i] - at(du, i) * b[i + 1] - at(dl, i) * b[i + 2]) / at(dd, i);
+}
+
+// one CTA: orthonormalise the m columns of y (n x m, ld ldy) by classical
+// Gram-Schmidt applied twice per column; r (m doubles) in dynamic shared memory.
+// A column that vanishes (dependent) is left at zero and reported in *bad.
+__global__ void __launch_bounds__(1024) k_cgs2(double* __restrict__ y, int64_t n, int64_t ldy, int64_t m,
+                                               int* __restrict__ bad) {
+  extern __shared__ double r[];
+  __shared__ double red[32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
+  for (int64_t j = 0; j < m; ++j) {
+    double* yj = y + j * ldy;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int64_t i = w; i < j; i += nw) {  // r_i = y_i . y_j, one warp per previous column
+        const double* yi = y + i * ldy;
+        double s = 0.0;
+        for (int64_t q = lane; q < n; q += 32) s += yi[q] * yj[q];
+        s = warp_sum(s);
+        if (lane == 0) r[i] = s;
+      }
+      __syncthreads();
+      for (int64_t q = t; q < n; q += blockDim.x) {
+        double v = yj[q];
+        for (int64_t i = 0; i < j; ++i) v -= r[i] * y[i * ldy + q];
+        yj[q] = v;
+      }
+      __syncthreads();
+    }
+    double s = 0.0;
+    for (int64_t q = t; q < n; q += blockDim.x) s += yj[q] * yj[q];
+    s = warp_sum(s);
+    if (lane == 0) red[w] = s;
+    __syncthreads();
+    if (t < 32) {
+      double v = t < nw ? red[t] : 0.0;
+      v = warp_sum(v);
+      if (t == 0) red[0] = v;
+    }
+    __syncthreads();
+    const double nrm = sqrt(red[0]);
+    const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+    if (nrm == 0.0 && t == 0) atomicAdd(bad, 1);
+    for (int64_t q = t; q < n; q += blockDim.x) yj[q] *= inv;
+    __syncthreads();
+  }
+}
 
 }  // namespace
 
-static void orthonormalize(Ctx& c, double* x, int64_t n, int64_t k) {
-  // Newton-Schulz: X <- X (1.5 I - 0.5 X^T X). Converges quadratically from the
-  // eps*||G||/gap non-orthogonality of independently computed eigenvectors.
+// W = X^T X (k x k, exactly symmetric) on the DMMA GEMM
+static void form_xtx(Ctx& c, const double* x, int64_t n, int64_t k, double* w) {
+  GemmDesc g;
+  g.M = k; g.N = k; g.K1 = n; g.K2 = 1;
+  g.A = x; g.ta = F64; g.sAm = n; g.sAk1 = 1;     // A(m,kk) = X(kk, m)
+  g.B = x; g.tb = F64; g.sBn = n; g.sBk1 = 1;     // B(kk,nn) = X(kk, nn)
+  g.C = w; g.sCm = 1; g.sCn = k;
+  g.syrk_upper = true;
+  gemm(c, g);
+  mirror_upper(c, w, k, 1, 0);
+}
+
+static double offidentity_host(Ctx& c, const double* w, int64_t k, double* chk) {
+  maxabs_offidentity(c, w, k, chk);
+  TMB_CUDA(cudaMemcpyAsync(c.host_pinned, chk, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  TMB_CUDA(cudaStreamSynchronize(c.stream));
+  return c.host_pinned[0];
+}
+
+// Above this max|X^T X - I| the vectors are not a small perturbation of an
+// orthonormal eigenbasis: a cluster was resolved as (nearly) parallel vectors.
+constexpr double kRepairOrtho = 1e-2;  // C2 solves measure up to 2e-4 (TMB_EIG_STATS)
+constexpr double kOrthoDone = 1e-13;
+
+// Newton-Schulz: X <- X (1.5 I - 0.5 X^T X), quadratically convergent from the
+// eps*||G||/gap non-orthogonality of independently computed eigenvectors,
+// repeated until max|X^T X - I| < 1e-13 (ENUMERIC if it does not get there).
+// Returns the initial max|X^T X - I| without iterating when it is >= `limit`.
+static double orthonormalize(Ctx& c, double* x, int64_t n, int64_t k, double limit) {
   const size_t mk = c.arena.mark();
   double* w = alloc<double>(c, (size_t)k * k);
   double* b = alloc<double>(c, (size_t)k * k);
   double* y = alloc<double>(c, (size_t)n * k);
   double* chk = alloc<double>(c, 1);
-  auto form_w = [&](const double* xx) {
-    GemmDesc g;
-    g.M = k; g.N = k; g.K1 = n; g.K2 = 1;
-    g.A = xx; g.ta = F64; g.sAm = n; g.sAk1 = 1;     // A(m,kk) = X(kk, m)
-    g.B = xx; g.tb = F64; g.sBn = n; g.sBk1 = 1;     // B(kk,nn) = X(kk, nn)
-    g.C = w; g.sCm = 1; g.sCn = k;
-    g.syrk_upper = true;
-    gemm(c, g);
-    mirror_upper(c, w, k, 1, 0);
-  };
-  form_w(x);
-  maxabs_offidentity(c, w, k, chk);
-  TMB_CUDA(cudaMemcpyAsync(c.host_pinned, chk, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-  TMB_CUDA(cudaStreamSynchronize(c.stream));
-  const double e0 = c.host_pinned[0];
-  if (!(e0 < 0.5)) {
+  form_xtx(c, x, n, k, w);
+  const double e0 = offidentity_host(c, w, k, chk);
+  if (!(e0 < limit)) {
     c.arena.release(mk);
-    throw Error(TMB_ENUMERIC, "leading_eigvecs: eigenvector solve lost orthogonality (clustered eigenvalues); "
-                              "max|X^T X - I| = " + std::to_string(e0));
+    return e0;
   }
-  int iters = e0 < 1e-14 ? 0 : (e0 < 1e-7 ? 1 : (e0 < 1e-3 ? 2 : 4));
+  double e = e0;
   double* cur = x;
   double* nxt = y;
-  for (int it = 0; it < iters; ++it) {
-    if (it > 0) form_w(cur);
+  for (int it = 0; e >= kOrthoDone; ++it) {
+    if (it >= 12) {
+      c.arena.release(mk);
+      throw Error(TMB_ENUMERIC, "leading_eigvecs: orthonormalisation did not converge, max|X^T X - I| = " +
+                                    std::to_string(e));
+    }
+    if (it > 0) form_xtx(c, cur, n, k, w);
     scale_identity_combo(c, w, k, 1.5, -0.5, b);
     GemmDesc g;
     g.M = n; g.N = k; g.K1 = k; g.K2 = 1;
@@ -946,9 +1084,72 @@ static void orthonormalize(Ctx& c, double* x, int64_t n, int64_t k) {
     g.C = nxt; g.sCm = 1; g.sCn = n;
     gemm(c, g);
     std::swap(cur, nxt);
+    // quadratic convergence: from e < 1e-7 one step lands below ~1.5e-14; otherwise re-measure
+    if (e < 1e-7) break;
+    form_xtx(c, cur, n, k, w);
+    e = offidentity_host(c, w, k, chk);
   }
   if (cur != x) copy_d(c, x, cur, n * k);
   c.arena.release(mk);
+  return e0;
+}
+
+// Replace the tridiagonal-basis vectors z (n x k) of every cluster of
+// (nearly) parallel columns by an orthonormal basis of the cluster's invariant
+// subspace (block inverse iteration). Clusters: connected components of
+// |z_i . z_j| > 1e-6, widened to contiguous index ranges (the eigenvalues are
+// sorted, so a cluster is a run of consecutive indices).
+static void repair_clusters(Ctx& c, const double* d, const double* e, int64_t n, int64_t k, const double* vals_dev,
+                            double* z) {
+  const size_t mk = c.arena.mark();
+  double* w = alloc<double>(c, (size_t)k * k);
+  form_xtx(c, z, n, k, w);
+  std::vector<double> hw((size_t)k * k), hv((size_t)k), hd((size_t)n), he((size_t)std::max<int64_t>(n - 1, 1));
+  TMB_CUDA(cudaMemcpyAsync(hw.data(), w, sizeof(double) * k * k, cudaMemcpyDeviceToHost, c.stream));
+  TMB_CUDA(cudaMemcpyAsync(hv.data(), vals_dev, sizeof(double) * k, cudaMemcpyDeviceToHost, c.stream));
+  TMB_CUDA(cudaMemcpyAsync(hd.data(), d, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+  if (n > 1) TMB_CUDA(cudaMemcpyAsync(he.data(), e, sizeof(double) * (n - 1), cudaMemcpyDeviceToHost, c.stream));
+  TMB_CUDA(cudaStreamSynchronize(c.stream));
+  double tnorm = 0.0;  // ||T||_inf, the scale of the zero-pivot perturbation
+  for (int64_t i = 0; i < n; ++i)
+    tnorm = std::max(tnorm, std::fabs(hd[i]) + (i > 0 ? std::fabs(he[i - 1]) : 0.0) +
+                                (i + 1 < n ? std::fabs(he[i]) : 0.0));
+  std::vector<int64_t> hi_of((size_t)k);  // furthest column coupled to column i
+  for (int64_t i = 0; i < k; ++i) {
+    hi_of[i] = i;
+    for (int64_t j = i + 1; j < k; ++j)
+      if (std::fabs(hw[(size_t)j * k + i]) > 1e-6) hi_of[i] = j;
+  }
+  int* bad = alloc<int>(c, 1);
+  TMB_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c.stream));
+  for (int64_t a = 0; a < k;) {
+    int64_t bnd = hi_of[a];
+    for (int64_t i = a; i <= bnd; ++i) bnd = std::max(bnd, hi_of[i]);
+    const int64_t m = bnd - a + 1;
+    if (m >= 2) {
+      const double sigma = 0.5 * (hv[a] + hv[bnd]);
+      const double pert = std::max(DBL_EPSILON * tnorm, DBL_MIN);
+      double* ya = z + a * n;
+      double* scr = alloc<double>(c, (size_t)3 * n * m);
+      k_fill_rand<<<(unsigned)std::min<int64_t>(ceil_div(n * m, 256), 4096), 256, 0, c.stream>>>(
+          ya, n, m, n, 0x5EEDull + (uint64_t)a);
+      LAUNCHED("k_fill_rand");
+      const size_t sm = sizeof(double) * (size_t)m;
+      set_smem_attr(c, (const void*)k_cgs2, std::max<size_t>(sm, 48 * 1024));
+      for (int it = 0; it < 3; ++it) {  // the cluster dominates (T - sigma)^-1 by gap/spread per step
+        k_tri_shift_solve<<<(unsigned)ceil_div(m, 128), 128, 0, c.stream>>>(d, e, n, sigma, pert, ya, n, m, scr);
+        LAUNCHED("k_tri_shift_solve");
+        k_cgs2<<<1, 1024, sm, c.stream>>>(ya, n, n, m, bad);
+        LAUNCHED("k_cgs2");
+      }
+    }
+    a = bnd + 1;
+  }
+  int hbad = 0;
+  TMB_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  TMB_CUDA(cudaStreamSynchronize(c.stream));
+  c.arena.release(mk);
+  if (hbad) throw Error(TMB_ENUMERIC, "leading_eigvecs: cluster inverse iteration lost rank");
 }
 
 // Reflectors per compact-WY panel: 64 (the fused k_apply_wy tile); TMB_WY_NB=32
@@ -1498,6 +1699,7 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
   double* dp = alloc<double>(c, (size_t)n * k);
   double* dm = alloc<double>(c, (size_t)n * k);
   double* zs = alloc<double>(c, (size_t)n * k);
+  std::function<void()> run_twisted;
   {
     Timed timed_tri(c, TAG_TRIDIAG, 0.0);
     // 2 warps (eigenvalues) per block: the counts are FP64-throughput bound, so
@@ -1512,17 +1714,35 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
     LAUNCHED("k_bisect");
     static const bool tw_global = std::getenv("TMB_TWISTED_GLOBAL") != nullptr;  // A/B: L2 scratch variant
     const size_t tw_smem = sizeof(double) * 2 * (size_t)n;  // per eigenvalue
-    if (!tw_global && tw_smem <= 200 * 1024) {
-      set_smem_attr(c, (const void*)k_twisted_sm, 200 * 1024);
-      k_twisted_sm<<<(unsigned)k, 64, tw_smem, c.stream>>>(d, e, n, k, vals, vecs);
-      LAUNCHED("k_twisted_sm");
-    } else {
-      k_twisted<<<(unsigned)ceil_div(k, 2), 64, 0, c.stream>>>(d, e, n, k, vals, dp, dm, zs, vecs);
-      LAUNCHED("k_twisted");
-    }
+    run_twisted = [&, tw_smem]() {
+      if (!tw_global && tw_smem <= 200 * 1024) {
+        set_smem_attr(c, (const void*)k_twisted_sm, 200 * 1024);
+        k_twisted_sm<<<(unsigned)k, 64, tw_smem, c.stream>>>(d, e, n, k, vals, vecs);
+        LAUNCHED("k_twisted_sm");
+      } else {
+        k_twisted<<<(unsigned)ceil_div(k, 2), 64, 0, c.stream>>>(d, e, n, k, vals, dp, dm, zs, vecs);
+        LAUNCHED("k_twisted");
+      }
+    };
+    run_twisted();
   }
   backtransform(c, hv, tau, n, hv_cols, k, vecs);
-  orthonormalize(c, vecs, n, k);
+  const double e0 = orthonormalize(c, vecs, n, k, kRepairOrtho);
+  static const bool stats = std::getenv("TMB_EIG_STATS") != nullptr;  // diagnostics: initial non-orthogonality
+  if (stats) std::fprintf(stderr, "leading_eigvecs n=%lld k=%lld max|X^T X - I| = %.3e\n", (long long)n,
+                          (long long)k, e0);
+  if (!(e0 < kRepairOrtho)) {
+    // clustered eigenvalues resolved as (nearly) parallel vectors: recompute the
+    // tridiagonal vectors, repair the clusters by block inverse iteration, redo
+    // the back-transformation (rare; the product configs never take this path)
+    run_twisted();
+    repair_clusters(c, d, e, n, k, vals, vecs);
+    backtransform(c, hv, tau, n, hv_cols, k, vecs);
+    const double e1 = orthonormalize(c, vecs, n, k, 0.5);
+    if (!(e1 < 0.5))
+      throw Error(TMB_ENUMERIC, "leading_eigvecs: eigenvectors lost orthogonality after cluster repair; "
+                                "max|X^T X - I| = " + std::to_string(e1));
+  }
   sign_fix(c, vecs, n, k);
   c.arena.release(mk);
 }

@@ -143,7 +143,10 @@ void ttm_dev(Ctx& c, const void* x, DType tx, const Dims& dims, int mode, const 
   // full passes over the tensor (>= 8 GFLOP) with the contracted mode not the first:
   // Ozaki int8 digit products on tcgen05 (measured at C2: mode 1 1.62 vs 1.96 ms on
   // DMMA; mode 0, whose tensor rows are K-contiguous, 1.53 vs 1.25 ms -> DMMA)
-  if (ozaki_enabled() && L >= 32 && 2.0 * (double)L * Rr * K * r >= 8e9 && K <= 65536) {
+  // (launch-grid limit: the digit split and GEMM grids have L*Rr/32 and L*Rr/64 rows in
+  // gridDim.y <= 65535; K < 65536 keeps 8*64*64*K digit products inside int32)
+  if (ozaki_enabled() && L >= 32 && 2.0 * (double)L * Rr * K * r >= 8e9 && K < 65536 &&
+      L * Rr <= 32LL * 65535 - 128) {
     ozaki_ttm(c, x, tx, L, K, Rr, m, r, sMr, sMk, y);
     return;
   }

@@ -181,6 +181,61 @@ def test_eig_large_n_vs_lapack(n, k):
     assert np.abs(v - vr).max() < 1e-8
 
 
+def _cluster_checks(g, k, v, w, clusters):
+    vr, wr = oracle.leading_eigvecs(g, k)
+    from conftest import principal_angle
+
+    scale = max(abs(wr[0]), 1.0)
+    assert np.abs(v.T @ v - np.eye(k)).max() < 1e-12
+    assert np.abs(w - wr).max() / scale < 1e-12
+    assert np.abs(g @ v - v * w).max() / scale < 1e-10
+    for a, b in clusters:   # a repeated eigenvalue's vectors are defined up to rotation: compare spans
+        assert principal_angle(v[:, a:b], vr[:, a:b]) < 1e-8
+
+
+def test_eig_repeated_eigenvalue_cluster():
+    """n > 64 with an exactly repeated eigenvalue (20-fold) inside the
+    wanted block -- the independently computed twisted vectors come out parallel
+    and the cluster is repaired by block inverse iteration."""
+    rng = np.random.default_rng(31)
+    n, k = 300, 60
+    lam = np.concatenate([np.linspace(50, 11, 10), np.full(20, 7.0), np.linspace(5, 0.1, n - 30)])
+    q = rand_orth(rng, n, n)
+    g = (q * lam) @ q.T
+    g = 0.5 * (g + g.T)
+    v, w = tb.leading_eigvecs(g, k)
+    _cluster_checks(g, k, v, w, [(10, 30)])
+
+
+def test_eig_rank_deficient_gram():
+    """A Gram of rank 40 asked for 100 eigenvectors (60 zero eigenvalues), n = 500."""
+    rng = np.random.default_rng(32)
+    b = rng.standard_normal((500, 40))
+    g = b @ b.T
+    v, w = tb.leading_eigvecs(g, 100)
+    vr, wr = oracle.leading_eigvecs(g, 100)
+    assert np.abs(v.T @ v - np.eye(100)).max() < 1e-12
+    assert np.abs(w - wr).max() / wr[0] < 1e-12
+    assert np.abs(g @ v - v * w).max() / wr[0] < 1e-12
+    from conftest import principal_angle
+
+    assert principal_angle(v[:, :40], vr[:, :40]) < 1e-9
+    # the 60 null-space vectors are orthogonal to the range of b
+    assert np.abs(b.T @ v[:, 40:]).max() < 1e-10 * np.abs(b).max()
+
+
+def test_hosvd_rank_deficient_modes():
+    """ADVICE r1 example: hosvd of a (100, 3, 3) tensor -- the mode-0 Gram has
+    rank <= 9 and all 100 eigenvectors are wanted; exact reconstruction and
+    orthonormal factors (tests/test_tucker.py:50-55 at n > 64)."""
+    rng = np.random.default_rng(33)
+    t = tb.DenseTensor(rng.standard_normal((100, 3, 3)))
+    model = tb.hosvd(t)
+    model.validate()
+    rec = tb.reconstruct(model)
+    assert np.abs(rec.array - t.array).max() < 1e-10
+
+
 def test_eig_deterministic():  # tests/test_tensor.py:218-223
     rng = np.random.default_rng(9)
     b = rng.standard_normal((300, 300))

@@ -137,6 +137,10 @@ int tmb_ttmc(tmb_ctx* ctx, const void* x_dev, int dtype, int order, const int64_
 /* gram (tensor.py:176-180): g = m m^T for column-major rows x cols m, exactly
  * symmetric (upper triangle computed, mirrored). */
 int tmb_gram(tmb_ctx* ctx, const double* m_dev, int64_t rows, int64_t cols, double* g_dev);
+/* g <- triu(g) + triu(g, 1)^T for a column-major n x n g (the exact symmetry
+ * of gram, tensor.py:176-180), for Grams assembled from separately computed
+ * blocks (the row-sharded solver's mode-0 Gram). */
+int tmb_mirror_upper(tmb_ctx* ctx, double* g_dev, int64_t n);
 /* gram(unfold(x, mode)) without materialising the unfolding. */
 int tmb_mode_gram(tmb_ctx* ctx, const void* x_dev, int dtype, int order, const int64_t* dims,
                   int mode, double* g_dev);

@@ -65,6 +65,7 @@ SIGNATURES = {
     "tmb_ttm": ([_vp, _vp, _int, _int, _pi64, _int, _vp, _i64, _vp], _int),
     "tmb_ttmc": ([_vp, _vp, _int, _int, _pi64, _pvp, _pi64, _pi64, _int, _int, _int, _vp], _int),
     "tmb_gram": ([_vp, _vp, _i64, _i64, _vp], _int),
+    "tmb_mirror_upper": ([_vp, _vp, _i64], _int),
     "tmb_mode_gram": ([_vp, _vp, _int, _int, _pi64, _int, _vp], _int),
     "tmb_leading_eigvecs": ([_vp, _vp, _i64, _i64, _vp, _vp], _int),
     "tmb_sumsq": ([_vp, _vp, _int, _i64, C.POINTER(_dbl)], _int),

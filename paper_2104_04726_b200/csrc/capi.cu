@@ -238,6 +238,13 @@ int tmb_gram(tmb_ctx* ctx, const double* m, int64_t rows, int64_t cols, double* 
   });
 }
 
+int tmb_mirror_upper(tmb_ctx* ctx, double* g, int64_t n) {
+  return guard(ctx, [&](tmb::Ctx& c) {
+    if (n < 1) throw Error(TMB_EINVAL, "mirror_upper: empty matrix");
+    tmb::mirror_upper(c, g, n, 1, 0);
+  });
+}
+
 int tmb_mode_gram(tmb_ctx* ctx, const void* x, int dtype, int order, const int64_t* dims, int mode, double* g) {
   return guard(ctx, [&](tmb::Ctx& c) {
     const Dims d = to_dims(order, dims);

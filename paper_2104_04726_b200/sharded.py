@@ -6,9 +6,14 @@ holds the mode-0 rows [r_i, r_{i+1}) of every (colour, view-exposure) plane and
 the solve exchanges one block per mode update, replacing the reference's
 single-process ``t_hosvd`` + ``hooi_sweep`` (tucker.py:130-163) with:
 
-* T-HOSVD: mode-0 Gram of the all-gathered row shards; modes n > 0 Grams are
-  additive over row shards (all-reduce); core = sum_i t_i x_0 S_0,i^T x_1 ...
-  (all-reduce of the partial core).
+* T-HOSVD: the mode-0 Gram by blocks -- the row shards are passed round the
+  ranks one at a time (a broadcast per shard), rank i forms its column block
+  G0[:, rows_i] = [T_j T_i^T]_j on the tensor pipe, and the column blocks are
+  all-gathered (no rank ever holds the whole tensor, and the 4320^2 Gram is
+  computed once, split G ways); modes n > 0 Grams are additive over row
+  shards (all-reduce); core = sum_i t_i x_0 S_0,i^T x_1 ... (all-reduce of
+  the partial core). The four T-HOSVD eigen-updates are independent, so mode
+  n is solved on rank n mod G and broadcast.
 * HOOI mode 0: Y0_i = t_i x_1 S_1^T x_2 S_2^T x_3 S_3^T is row-local; all-gather
   the rows, Gram and eigen-update replicated.
 * HOOI modes 1..3 and the core: A_i = t_i x_0 S_0,i^T is a partial sum over
@@ -17,8 +22,8 @@ single-process ``t_hosvd`` + ``hooi_sweep`` (tucker.py:130-163) with:
   Y3 x_3 S_3^T locally. The Gauss-Seidel order of the reference is kept (each
   factor is replaced before the next mode).
 
-Grams and eigen-updates are computed redundantly on every rank from bitwise
-identical all-reduced inputs (ring collectives hand every rank the same
+The HOOI Grams and eigen-updates (sequential in the Gauss-Seidel order) are
+computed redundantly on every rank from bitwise identical all-reduced inputs (ring collectives hand every rank the same
 bits; the eigen-solver is deterministic), so all ranks hold identical factors.
 The driver reproduces tucker_als's trace, fit, best-of and |dfit| < fit_tol
 rules for standard sweeps; PP (pp_enter_tol > 0) is not sharded.
@@ -76,6 +81,11 @@ class TorchComm:
         self._dist.all_gather(out, t.contiguous(), group=self.group)
         return out
 
+    def broadcast(self, t, src: int):
+        self._dist.broadcast(t, src=self._dist.get_global_rank(self.group, src) if self.group else src,
+                             group=self.group)
+        return t
+
 
 class ThreadComm:
     """In-process ranks (one host thread each) for single-GPU emulation: every
@@ -119,6 +129,15 @@ class ThreadComm:
         self._sync()
         return out
 
+    def broadcast(self, t, src: int):
+        if self.rank == src:
+            self._slots[src] = t.clone()
+        self._sync()
+        if self.rank != src:
+            t.copy_(self._slots[src])
+        self._sync()
+        return t
+
 
 class DeviceOps:
     """The per-rank arithmetic through the libtmb C ABI on CUDA tensors (F-order flat)."""
@@ -155,6 +174,28 @@ class DeviceOps:
         g = torch.empty(n * n, dtype=torch.float64, device=x.device)
         h = L.ctx()
         L.check(L.LIB.tmb_mode_gram(h, L.ptr(x), self._dt(x), len(dims), L.i64s(dims), mode, L.ptr(g)), h)
+        return g
+
+    def cross_rows(self, xj, hj: int, xi64, hi: int, kdim: int):
+        """X_j X_i^T (hj x hi, column-major) of two mode-0 row blocks given as
+        F-order (h, K) matrices; xi64 float64 (the GEMM's factor operand)."""
+        import torch
+
+        L = self.L
+        y = torch.empty(hj * hi, dtype=torch.float64, device=xj.device)
+        h = L.ctx()
+        L.check(L.LIB.tmb_ttm(h, L.ptr(xj), self._dt(xj), 2, L.i64s((hj, kdim)), 1, L.ptr(xi64), hi, L.ptr(y)), h)
+        return y
+
+    def to_f64(self, x):
+        return x if self._dt(x) == self.L.F64 else x.double()
+
+    def mirror_upper(self, g, n: int):
+        """g <- triu(g) + triu(g, 1)^T in place: the exactly symmetric Gram of
+        gram() (tensor.py:176-180) from independently computed blocks."""
+        L = self.L
+        h = L.ctx()
+        L.check(L.LIB.tmb_mirror_upper(h, L.ptr(g), n), h)
         return g
 
     def eig(self, g, n: int, k: int):
@@ -198,6 +239,32 @@ def _gather_rows(comm, y, dims_local: Sequence[int], ranges) -> tuple:
     full = torch.cat([p[:, : b - a] for p, (a, b) in zip(parts, ranges)], dim=1)
     h = ranges[-1][1]
     return full.contiguous().view(-1), (h,) + tuple(dims_local[1:])
+
+
+def _blocked_mode0_gram(comm, ops, x_local, dims, ranges):
+    """Mode-0 Gram of a row-sharded tensor without gathering it: shard j is
+    broadcast in turn, rank i forms the block X_j X_i^T of its column block
+    G0[:, rows_i], the column blocks are all-gathered, and the upper triangle
+    is mirrored (the reference's exactly symmetric gram, tensor.py:176-180)."""
+    import torch
+
+    n = dims[0]
+    kdim = int(np.prod(dims[1:]))
+    a0, b0 = ranges[comm.rank]
+    hi = b0 - a0
+    xi64 = ops.to_f64(x_local)
+    hmax = max(b - a for a, b in ranges)
+    col = torch.empty((hmax, n), dtype=torch.float64, device=x_local.device)  # C-order (hi, n) = column-major n x hi
+    for j, (aj, bj) in enumerate(ranges):
+        hj = bj - aj
+        buf = x_local if j == comm.rank else torch.empty(hj * kdim, dtype=x_local.dtype, device=x_local.device)
+        comm.broadcast(buf, j)
+        y = ops.cross_rows(buf, hj, xi64, hi, kdim)                  # (hj x hi) column-major
+        col[:hi, aj:bj] = y.view(hi, hj)                              # rows aj..bj of columns rows_i
+        del buf
+    parts = comm.allgather(col.contiguous().view(-1))
+    g = torch.cat([p.view(hmax, n)[: b - a] for p, (a, b) in zip(parts, ranges)], dim=0).contiguous().view(-1)
+    return ops.mirror_upper(g, n)
 
 
 def _rows_of(u, s: int, r: int, a: int, b: int):
@@ -248,12 +315,17 @@ def sharded_tucker_als(x_local, dims: Sequence[int], cfg: SolveConfig, comm, ops
         return ops.ttm_t(y3, (r[0], r[1], r[2], s[3]), 3, u3, r[3])[0]
 
     # ---- T-HOSVD (tucker.py:130-148)
-    xf, _ = _gather_rows(comm, x_local, dl, ranges)
-    u = [ops.eig(ops.gram(xf, dims, 0), s[0], r[0])]
-    del xf
-    for n in (1, 2, 3):
-        g = comm.allreduce_sum(ops.gram(x_local, dl, n))
-        u.append(ops.eig(g, s[n], r[n]))
+    g0 = _blocked_mode0_gram(comm, ops, x_local, dims, ranges)
+    grams = [g0] + [comm.allreduce_sum(ops.gram(x_local, dl, n)) for n in (1, 2, 3)]
+    u = []
+    for n in range(4):   # independent eigen-updates: mode n on rank n mod G, then broadcast
+        owner = n % comm.world
+        if comm.rank == owner:
+            v = ops.eig(grams[n], s[n], r[n])
+        else:
+            v = torch.empty(s[n] * r[n], dtype=torch.float64, device=x_local.device)
+        u.append(comm.broadcast(v, owner))
+    del grams, g0
     p, pd = ops.ttm_t(x_local, dl, 0, _rows_of(u[0], s[0], r[0], a0, b0), r[0])
     for n in (1, 2):
         p, pd = ops.ttm_t(p, pd, n, u[n], r[n])

@@ -54,6 +54,19 @@ class OracleOps:
     def gram(self, x, dims, mode):
         return self._flat(self.O.gram(self.O.unfold(self._arr(x, dims), mode)))
 
+    def cross_rows(self, xj, hj, xi64, hi, kdim):
+        a = xj.numpy().astype(np.float64).reshape((hj, kdim), order="F")
+        b = xi64.numpy().reshape((hi, kdim), order="F")
+        return self._flat(a @ b.T)
+
+    def to_f64(self, x):
+        return x.double()
+
+    def mirror_upper(self, g, n):
+        m = g.numpy().reshape((n, n), order="F")
+        m = np.triu(m) + np.triu(m, 1).T
+        return self._flat(m)
+
     def eig(self, g, n, k):
         v, _ = self.O.leading_eigvecs(g.numpy().reshape((n, n), order="F"), k)
         return self._flat(v)
@@ -178,3 +191,63 @@ def test_two_thread_ranks_on_device_match_unsharded():
         assert principal_angle(a, b) < 1e-6
     for r0, r1 in zip(tr0.records, ref_trace.records):
         assert abs(r0.fit - r1.fit) < 1e-10
+
+
+def _device_worker(rank: int, world: int, port: int, q):
+    """One process per rank on the SAME GPU, the product's TorchComm (gloo on CUDA
+    tensors -- NCCL refuses two ranks on one device) + DeviceOps (libtmb)."""
+    import torch.distributed as dist
+
+    import paper_2104_04726_b200 as tb
+    from paper_2104_04726_b200.pipeline import coding_tensor
+    from paper_2104_04726_b200.sharded import DeviceOps, TorchComm, sharded_tucker_als
+    from paper_2104_04726_b200.synth import CONFIGS, make_stack
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg0 = CONFIGS["c1"]
+    t = coding_tensor(make_stack(cfg0, seed=2), cfg0.space)
+    dims = tuple(int(d) for d in cfg0.dims)
+    full = t.view(int(np.prod(dims[1:])), dims[0])
+    a, b = row_ranges(dims[0], world)[rank]
+    xl = full[:, a:b].contiguous().view(-1)
+    sc = tb.SolveConfig(ranks=cfg0.ranks, max_sweeps=3, fit_tol=1e-300, pp_enter_tol=0.0)
+    model, trace = sharded_tucker_als(xl, dims, sc, TorchComm(), DeviceOps())
+    q.put((rank, [f.copy() for f in model.factors], [r.fit for r in trace.records]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_process_ranks_torchcomm_deviceops_match_unsharded():
+    import paper_2104_04726_b200 as tb
+    from paper_2104_04726_b200.pipeline import coding_tensor
+    from paper_2104_04726_b200.synth import CONFIGS, make_stack
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_device_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    (_, f0, fit0), (_, f1, fit1) = out
+    for a, b in zip(f0, f1):
+        assert np.array_equal(a, b)          # every rank holds the same model
+    assert fit0 == fit1
+    cfg0 = CONFIGS["c1"]
+    t = coding_tensor(make_stack(cfg0, seed=2), cfg0.space)
+    dims = tuple(int(d) for d in cfg0.dims)
+    sc = tb.SolveConfig(ranks=cfg0.ranks, max_sweeps=3, fit_tol=1e-300, pp_enter_tol=0.0)
+    ref_model, ref_trace = tb.tucker.solve_device(t, tb._lib.F32, dims, sc)
+    from conftest import principal_angle
+
+    for a, b in zip(f0, ref_model.factors):
+        assert principal_angle(a, b) < 1e-6
+    for x, y in zip(fit0, [r.fit for r in ref_trace.records]):
+        assert abs(x - y) < 1e-10

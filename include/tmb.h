@@ -188,6 +188,35 @@ int tmb_solve_channels(tmb_ctx* ctx, const void* x_dev, int dtype, const int64_t
                        const tmb_solve_cfg* cfg, double* const* cores_dev, double* const* factors_dev,
                        tmb_trace* traces);
 
+/* Pairwise perturbation (tucker.py:199-311) as a native handle owning the
+ * dimension-tree operators on the device.
+ *  tmb_pp_operators : pp_operators (tucker.py:222-265), the memoised dimension
+ *                     tree (parent = re-add the largest contracted mode, so
+ *                     every node is an ascending contraction; 13 contractions
+ *                     for N = 4), anchors[n] column-major dims[n] x ranks[n].
+ *  tmb_pp_operator  : device pointer + dims of the operator whose free modes
+ *                     are `free_mask` (op_single: 1<<n, pair(i, n): 1<<i|1<<n),
+ *                     owned by the handle.
+ *  tmb_pp_operator_copy: the same operator copied into a caller buffer.
+ *  tmb_pp_set_deltas: PPState.set_current (src_are_factors = 1: d = f - a) or
+ *                     PPState.deltas = src (0); returns max_rel_delta
+ *                     (tucker.py:212-219).
+ *  tmb_pp_sweep     : pp_sweep (tucker.py:285-311) from the stored deltas:
+ *                     factors_dev[n] receive the new factors, core_dev (nullable)
+ *                     the pp core estimate, operands_dev[n] (nullable array /
+ *                     entries) the first-order operands. */
+typedef struct tmb_pp tmb_pp;
+int tmb_pp_operators(tmb_ctx* ctx, const void* x_dev, int dtype, int order, const int64_t* dims,
+                     const int64_t* ranks, const double* const* anchors_dev, tmb_pp** out);
+int tmb_pp_info(const tmb_pp* pp, int* order, int* contraction_count);
+int tmb_pp_operator(const tmb_pp* pp, unsigned free_mask, const double** op_dev, int64_t* dims_out);
+int tmb_pp_operator_copy(tmb_ctx* ctx, const tmb_pp* pp, unsigned free_mask, double* out_dev);
+int tmb_pp_set_deltas(tmb_ctx* ctx, tmb_pp* pp, const double* const* src_dev, int src_are_factors,
+                      double* max_rel_delta_host);
+int tmb_pp_sweep(tmb_ctx* ctx, tmb_pp* pp, double* core_dev, double* const* factors_dev,
+                 double* const* operands_dev);
+int tmb_pp_destroy(tmb_pp* pp);
+
 /* ---- codec (codec.py) --------------------------------------------------- */
 /* quantize_core (codec.py:114-134): int64 levels, step returned to host. */
 int tmb_quantize_core(tmb_ctx* ctx, const double* core_dev, int64_t n, int qp,

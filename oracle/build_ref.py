@@ -27,6 +27,8 @@ from pathlib import Path
 REF_PKG = Path("/root/reference/pkg")
 OUT = Path(__file__).resolve().parent / "_ref"
 STAMP = OUT / ".built_from"
+REF_TESTS = ("conftest.py", "test_tensor.py", "test_tucker.py", "test_pp.py", "test_color.py", "test_codec.py",
+             "test_metrics.py")
 
 
 def _source_mtime() -> float:
@@ -37,7 +39,7 @@ def build(force: bool = False) -> Path | None:
     """Install the reference into oracle/_ref; returns the path (None if unavailable)."""
     if not REF_PKG.exists():
         return OUT if (OUT / "tmcodec").exists() else None
-    if not force and STAMP.exists() and (OUT / "tmcodec").exists():
+    if not force and STAMP.exists() and (OUT / "tmcodec").exists() and (OUT / "reference_tests").exists():
         try:
             if float(STAMP.read_text().split()[0]) >= _source_mtime():
                 return OUT
@@ -55,6 +57,12 @@ def build(force: bool = False) -> Path | None:
         if OUT.exists():
             shutil.rmtree(OUT)
         shutil.copytree(staging, OUT, ignore=shutil.ignore_patterns("__pycache__", "bin"))
+        # the reference's own unit tests for the hot-path modules, run UNCHANGED against
+        # the drop-in by tests/test_reference_suite.py
+        tdir = OUT / "reference_tests"
+        tdir.mkdir()
+        for name in REF_TESTS:
+            shutil.copy2(REF_PKG / "tests" / name, tdir / name)
     STAMP.write_text(f"{_source_mtime()} {REF_PKG}\n")
     return OUT
 

@@ -65,6 +65,13 @@ SIGNATURES = {
     "tmb_ttm": ([_vp, _vp, _int, _int, _pi64, _int, _vp, _i64, _vp], _int),
     "tmb_ttmc": ([_vp, _vp, _int, _int, _pi64, _pvp, _pi64, _pi64, _int, _int, _int, _vp], _int),
     "tmb_gram": ([_vp, _vp, _i64, _i64, _vp], _int),
+    "tmb_pp_operators": ([_vp, _vp, _int, _int, _pi64, _pi64, _pvp, C.POINTER(_vp)], _int),
+    "tmb_pp_info": ([_vp, C.POINTER(_int), C.POINTER(_int)], _int),
+    "tmb_pp_operator": ([_vp, C.c_uint, C.POINTER(_vp), _pi64], _int),
+    "tmb_pp_operator_copy": ([_vp, _vp, C.c_uint, _vp], _int),
+    "tmb_pp_set_deltas": ([_vp, _vp, _pvp, _int, C.POINTER(_dbl)], _int),
+    "tmb_pp_sweep": ([_vp, _vp, _vp, _pvp, _pvp], _int),
+    "tmb_pp_destroy": ([_vp], _int),
     "tmb_mirror_upper": ([_vp, _vp, _i64], _int),
     "tmb_mode_gram": ([_vp, _vp, _int, _int, _pi64, _int, _vp], _int),
     "tmb_leading_eigvecs": ([_vp, _vp, _i64, _i64, _vp, _vp], _int),

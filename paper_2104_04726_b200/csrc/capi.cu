@@ -9,6 +9,11 @@ struct tmb_ctx {
   tmb::Ctx c;
 };
 
+struct tmb_pp {
+  tmb::PPOps ops;
+  int device = 0;
+};
+
 namespace {
 
 using tmb::Dims;
@@ -363,6 +368,78 @@ int tmb_channels_to_rgb(tmb_ctx* ctx, const double* t, int64_t n_img, int64_t h,
     if (n_img < 0 || h < 0 || w < 0) throw Error(TMB_EINVAL, "negative image dimensions");
     tmb::channels_to_rgb(c, t, n_img, h, w, space, rgb);
   });
+}
+
+int tmb_pp_operators(tmb_ctx* ctx, const void* x, int dtype, int order, const int64_t* dims, const int64_t* ranks,
+                     const double* const* anchors, tmb_pp** out) {
+  if (!out) return TMB_EINVAL;
+  *out = nullptr;
+  return guard(ctx, [&](tmb::Ctx& c) {
+    const Dims d = to_dims(order, dims);
+    const Dims r = check_ranks(d, ranks);
+    if (order > 16 || !anchors) throw Error(TMB_EINVAL, "expected " + std::to_string(order) + " anchors");
+    auto* h = new tmb_pp;
+    h->device = c.device;
+    try {
+      tmb::pp_build(c, h->ops, x, to_dtype(dtype), d, r, anchors);
+      TMB_CUDA(cudaStreamSynchronize(c.stream));
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int tmb_pp_info(const tmb_pp* pp, int* order, int* contraction_count) {
+  if (!pp) return TMB_EINVAL;
+  if (order) *order = (int)pp->ops.dims.size();
+  if (contraction_count) *contraction_count = pp->ops.count;
+  return TMB_OK;
+}
+
+int tmb_pp_operator(const tmb_pp* pp, unsigned free_mask, const double** op_dev, int64_t* dims_out) {
+  if (!pp || !op_dev) return TMB_EINVAL;
+  const double* p = pp->ops.find(free_mask);
+  if (!p) return TMB_EINVAL;
+  *op_dev = p;
+  if (dims_out) {
+    const Dims d = tmb::pp_node_dims(pp->ops.dims, pp->ops.ranks, free_mask);
+    for (size_t n = 0; n < d.size(); ++n) dims_out[n] = d[n];
+  }
+  return TMB_OK;
+}
+
+int tmb_pp_operator_copy(tmb_ctx* ctx, const tmb_pp* pp, unsigned free_mask, double* out) {
+  return guard(ctx, [&](tmb::Ctx& c) {
+    if (!pp || !out) throw Error(TMB_EINVAL, "null pp state or output");
+    const double* p = pp->ops.find(free_mask);
+    if (!p) throw Error(TMB_EINVAL, "no pp operator for free-mode mask " + std::to_string(free_mask));
+    const Dims d = tmb::pp_node_dims(pp->ops.dims, pp->ops.ranks, free_mask);
+    tmb::copy_d(c, out, p, tmb::prod(d, 0, (int)d.size()));
+  });
+}
+
+int tmb_pp_set_deltas(tmb_ctx* ctx, tmb_pp* pp, const double* const* src, int src_are_factors, double* max_rel) {
+  return guard(ctx, [&](tmb::Ctx& c) {
+    if (!pp || !src) throw Error(TMB_EINVAL, "null pp state or inputs");
+    const double m = tmb::pp_set_deltas(c, pp->ops, src, src_are_factors != 0);
+    if (max_rel) *max_rel = m;
+  });
+}
+
+int tmb_pp_sweep(tmb_ctx* ctx, tmb_pp* pp, double* core, double* const* factors, double* const* operands) {
+  return guard(ctx, [&](tmb::Ctx& c) {
+    if (!pp || !factors) throw Error(TMB_EINVAL, "null pp state or outputs");
+    tmb::pp_sweep_dev(c, pp->ops, factors, core, operands);
+  });
+}
+
+int tmb_pp_destroy(tmb_pp* pp) {
+  if (!pp) return TMB_OK;
+  cudaSetDevice(pp->device);
+  delete pp;
+  return TMB_OK;
 }
 
 int tmb_quantize_core(tmb_ctx* ctx, const double* core, int64_t n, int qp, int64_t* levels, double* step_host) {

@@ -349,34 +349,9 @@ void reconstruct_dev(Ctx& c, const Dims& ranks, const Dims& dims, const double* 
 // ------------------------------------------------------------------ pairwise perturbation
 // tucker.py:199-311. Operators persist across sweeps (own cudaMalloc buffers,
 // outside the per-sweep arena); rebuilt only when the PP phase refreshes.
-struct DevBuf {
-  double* p = nullptr;
-  DevBuf() = default;
-  explicit DevBuf(size_t count) {
-    TMB_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double)));
-  }
-  ~DevBuf() { if (p) cudaFree(p); }
-  DevBuf(DevBuf&& o) noexcept : p(o.p) { o.p = nullptr; }
-  DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { if (p) cudaFree(p); p = o.p; o.p = nullptr; }
-    return *this;
-  }
-  DevBuf(const DevBuf&) = delete;
-  DevBuf& operator=(const DevBuf&) = delete;
-};
+// PPOps / DevBuf are declared in solver.h (the C ABI's tmb_pp handle wraps one).
 
-struct PPOps {
-  std::vector<DevBuf> anchors;          // device copies of the anchor factors
-  std::vector<std::pair<unsigned, DevBuf>> nodes;  // free-mode bitmask -> operator
-  int count = 0;                        // contractions evaluated (13 for N = 4)
-  const double* find(unsigned m) const {
-    for (const auto& kv : nodes)
-      if (kv.first == m) return kv.second.p;
-    return nullptr;
-  }
-};
-
-static Dims node_dims(const Dims& dims, const Dims& ranks, unsigned free_modes) {
+Dims pp_node_dims(const Dims& dims, const Dims& ranks, unsigned free_modes) {
   Dims d(dims.size());
   for (size_t n = 0; n < dims.size(); ++n) d[n] = ((free_modes >> n) & 1u) ? dims[n] : ranks[n];
   return d;
@@ -384,70 +359,116 @@ static Dims node_dims(const Dims& dims, const Dims& ranks, unsigned free_modes) 
 
 // Memoised dimension tree: the parent of a node re-adds its largest contracted
 // mode, so every node is an ascending contraction (tucker.py:238-252).
-static std::pair<const void*, DType> pp_node(Ctx& c, PPOps& ops, const void* x, DType tx, const Dims& dims,
-                                             const Dims& ranks, unsigned free_modes) {
+static std::pair<const void*, DType> pp_node(Ctx& c, PPOps& ops, const void* x, DType tx, unsigned free_modes) {
+  const Dims& dims = ops.dims;
+  const Dims& ranks = ops.ranks;
   const int N = (int)dims.size();
   const unsigned all = (1u << N) - 1u;
   if (free_modes == all) return {x, tx};
   if (const double* got = ops.find(free_modes)) return {got, F64};
+  if (!x) throw Error(TMB_EINVAL, "pp operator " + std::to_string(free_modes) + " was not built");
   int m = N - 1;
   while ((free_modes >> m) & 1u) --m;
-  const auto parent = pp_node(c, ops, x, tx, dims, ranks, free_modes | (1u << m));
-  DevBuf out((size_t)prod(node_dims(dims, ranks, free_modes), 0, N));
-  ttm_dev(c, parent.first, parent.second, node_dims(dims, ranks, free_modes | (1u << m)), m, ops.anchors[m].p,
+  const auto parent = pp_node(c, ops, x, tx, free_modes | (1u << m));
+  DevBuf out((size_t)prod(pp_node_dims(dims, ranks, free_modes), 0, N));
+  ttm_dev(c, parent.first, parent.second, pp_node_dims(dims, ranks, free_modes | (1u << m)), m, ops.anchors[m].p,
           ranks[m], dims[m], 1, out.p);
   ops.count++;
   ops.nodes.emplace_back(free_modes, std::move(out));
   return {ops.nodes.back().second.p, F64};
 }
 
-static void pp_build(Ctx& c, PPOps& ops, const void* x, DType tx, const Dims& dims, const Dims& ranks,
-                     const std::vector<double*>& anchors) {
+// pp_operators (tucker.py:222-265): every skip-one and skip-two operator
+void pp_build(Ctx& c, PPOps& ops, const void* x, DType tx, const Dims& dims, const Dims& ranks,
+              const double* const* anchors) {
   const int N = (int)dims.size();
+  ops.dims = dims;
+  ops.ranks = ranks;
   ops.nodes.clear();
   ops.anchors.clear();
+  ops.deltas.clear();
+  ops.nonzero.assign(N, 0);
   ops.count = 0;
   for (int n = 0; n < N; ++n) {
     ops.anchors.emplace_back((size_t)dims[n] * ranks[n]);
     copy_d(c, ops.anchors.back().p, anchors[n], dims[n] * ranks[n]);
+    ops.deltas.emplace_back((size_t)dims[n] * ranks[n]);
+    TMB_CUDA(cudaMemsetAsync(ops.deltas.back().p, 0, sizeof(double) * dims[n] * ranks[n], c.stream));
   }
-  for (int n = 0; n < N; ++n) pp_node(c, ops, x, tx, dims, ranks, 1u << n);                  // op_single
+  for (int n = 0; n < N; ++n) pp_node(c, ops, x, tx, 1u << n);                  // op_single
   for (int i = 0; i < N; ++i)
-    for (int n = i + 1; n < N; ++n) pp_node(c, ops, x, tx, dims, ranks, (1u << i) | (1u << n));  // op_pair
+    for (int n = i + 1; n < N; ++n) pp_node(c, ops, x, tx, (1u << i) | (1u << n));  // op_pair
 }
 
-// First-order sweep from the entry deltas (tucker.py:268-311): factors only;
-// the driver re-projects the exact core.
-static void pp_sweep_dev(Ctx& c, PPOps& ops, const void* x, DType tx, const Dims& dims, const Dims& ranks,
-                         const std::vector<double*>& fin, const std::vector<bool>& nonzero,
-                         const std::vector<double*>& fout) {
+// PPState.set_current (tucker.py:212-213: deltas = factors - anchors) when
+// `factors` is true, else the deltas themselves are given (PPState.deltas = ...);
+// returns max_rel_delta (tucker.py:215-219) and records which deltas are nonzero.
+double pp_set_deltas(Ctx& c, PPOps& ops, const double* const* src, bool factors) {
+  const int N = (int)ops.dims.size();
+  const size_t mk = c.arena.mark();
+  double* sc = alloc<double>(c, 2 * (size_t)N);
+  for (int n = 0; n < N; ++n) {
+    const int64_t cnt = ops.dims[n] * ops.ranks[n];
+    copy_d(c, ops.deltas[n].p, src[n], cnt);
+    if (factors) axpy(c, cnt, -1.0, ops.anchors[n].p, ops.deltas[n].p);
+    sumsq_async(c, ops.deltas[n].p, F64, cnt, sc + 2 * n);
+    sumsq_async(c, ops.anchors[n].p, F64, cnt, sc + 2 * n + 1);
+  }
+  std::vector<double> h(2 * (size_t)N);
+  TMB_CUDA(cudaMemcpyAsync(h.data(), sc, sizeof(double) * 2 * N, cudaMemcpyDeviceToHost, c.stream));
+  TMB_CUDA(cudaStreamSynchronize(c.stream));
+  c.arena.release(mk);
+  double out = 0.0;
+  for (int n = 0; n < N; ++n) {
+    ops.nonzero[n] = h[2 * n] > 0.0 ? 1 : 0;  // np.any(d) (tucker.py:275)
+    out = std::max(out, std::sqrt(h[2 * n]) / std::sqrt(h[2 * n + 1]));
+  }
+  return out;
+}
+
+// pp_sweep (tucker.py:285-311) from the stored entry deltas: operand
+// Y_n = op_single[n] + sum_{i != n, d_i != 0} pair(i, n) x_i d_i^T, the
+// corrections summed first in ascending i and then added to op_single
+// (_pp_operand, tucker.py:268-282, in the reference's order), then the
+// leading eigenvectors of its mode-n Gram; core = Y_{N-1} x_{N-1} S_{N-1}^T
+// when core_out is given (the pp estimate), operands copied out when given.
+void pp_sweep_dev(Ctx& c, PPOps& ops, double* const* fout, double* core_out, double* const* operands_out) {
+  const Dims& dims = ops.dims;
+  const Dims& ranks = ops.ranks;
   const int N = (int)dims.size();
   const size_t mk = c.arena.mark();
-  std::vector<double*> delta(N);
-  for (int i = 0; i < N; ++i) {  // d_i = f_i - a_i
-    const int64_t cnt = dims[i] * ranks[i];
-    delta[i] = alloc<double>(c, (size_t)cnt);
-    copy_d(c, delta[i], fin[i], cnt);
-    axpy(c, cnt, -1.0, ops.anchors[i].p, delta[i]);
-  }
+  const double* last_y = nullptr;
+  Dims last_d;
   for (int n = 0; n < N; ++n) {
-    const Dims yd = node_dims(dims, ranks, 1u << n);
+    const Dims yd = pp_node_dims(dims, ranks, 1u << n);
     const int64_t ysz = prod(yd, 0, N);
-    double* y = alloc<double>(c, (size_t)ysz);
-    copy_d(c, y, static_cast<const double*>(pp_node(c, ops, x, tx, dims, ranks, 1u << n).first), ysz);
+    const double* single = ops.find(1u << n);
+    if (!single) throw Error(TMB_EINVAL, "pp operators not built");
+    double* acc = nullptr;
     double* tmp = alloc<double>(c, (size_t)ysz);
     for (int i = 0; i < N; ++i) {
-      if (i == n || !nonzero[i]) continue;
+      if (i == n || !ops.nonzero[i]) continue;
       const unsigned pm = (1u << i) | (1u << n);
-      const double* pair = static_cast<const double*>(pp_node(c, ops, x, tx, dims, ranks, pm).first);
-      ttm_dev(c, pair, F64, node_dims(dims, ranks, pm), i, delta[i], ranks[i], dims[i], 1, tmp);  // x_i d_i^T
-      axpy(c, ysz, 1.0, tmp, y);
+      const double* pair = ops.find(pm);
+      double* dst = acc ? tmp : alloc<double>(c, (size_t)ysz);
+      ttm_dev(c, pair, F64, pp_node_dims(dims, ranks, pm), i, ops.deltas[i].p, ranks[i], dims[i], 1, dst);  // x_i d_i^T
+      if (acc) axpy(c, ysz, 1.0, tmp, acc);
+      else acc = dst;
     }
+    const double* y = single;
+    if (acc) {
+      axpy(c, ysz, 1.0, single, acc);  // y + acc (fp addition is commutative)
+      y = acc;
+    }
+    if (operands_out && operands_out[n]) copy_d(c, operands_out[n], y, ysz);
     double* G = alloc<double>(c, (size_t)dims[n] * dims[n]);
     double* vals = alloc<double>(c, (size_t)ranks[n]);
     mode_gram_dev(c, y, F64, yd, n, G);
     leading_eigvecs(c, G, dims[n], ranks[n], fout[n], vals);
+    last_y = y;
+    last_d = yd;
   }
+  if (core_out) ttm_dev(c, last_y, F64, last_d, N - 1, fout[N - 1], ranks[N - 1], dims[N - 1], 1, core_out);
   c.arena.release(mk);
 }
 
@@ -516,16 +537,9 @@ void tucker_als_dev(Ctx& c, const void* x, DType tx, const Dims& dims, const Dim
     int kind = TMB_KIND_STANDARD;
     bool have_candidate = false;
     if (phase_pp) {  // tucker.py:359-371
-      for (int n = 0; n < N; ++n) diff_norms(c, (*fc)[n], pp.anchors[n].p, dims[n] * ranks[n], scal + 2 + 2 * n);
-      read_scalars(2 + 2 * N);
-      double max_rel = 0.0;
-      std::vector<bool> nonzero(N);
-      for (int n = 0; n < N; ++n) {
-        nonzero[n] = c.host_pinned[2 + 2 * n] > 0.0;
-        max_rel = std::max(max_rel, std::sqrt(c.host_pinned[2 + 2 * n]) / std::sqrt(c.host_pinned[3 + 2 * n]));
-      }
+      const double max_rel = pp_set_deltas(c, pp, fc->data(), true);  // set_current + max_rel_delta
       if (max_rel <= cfg.pp_exit_tol) {
-        pp_sweep_dev(c, pp, x, tx, dims, ranks, *fc, nonzero, *fn);
+        pp_sweep_dev(c, pp, fn->data(), nullptr, nullptr);
         ttmc_dev(c, x, tx, dims, fn->data(), frows.data(), fcols.data(), -1, true, greedy, cn);  // _exact_core
         sumsq_async(c, cn, F64, Pc, scal);
         read_scalars(1);
@@ -535,7 +549,7 @@ void tucker_als_dev(Ctx& c, const void* x, DType tx, const Dims& dims, const Dim
         kind = TMB_KIND_PP;
       } else {  // drifted or regressed: refresh with a standard sweep and new anchors
         hooi_sweep_dev(c, x, tx, dims, ranks, fc->data(), greedy, cn, fn->data());
-        pp_build(c, pp, x, tx, dims, ranks, *fn);
+        pp_build(c, pp, x, tx, dims, ranks, fn->data());
       }
     } else {
       hooi_sweep_dev(c, x, tx, dims, ranks, fc->data(), greedy, cn, fn->data());  // tucker.py:373
@@ -557,7 +571,7 @@ void tucker_als_dev(Ctx& c, const void* x, DType tx, const Dims& dims, const Dim
     }
     if (kind == TMB_KIND_STANDARD && !phase_pp && cfg.pp_enter_tol > 0 && change < cfg.pp_enter_tol) {
       phase_pp = true;  // tucker.py:385-387
-      pp_build(c, pp, x, tx, dims, ranks, *fn);
+      pp_build(c, pp, x, tx, dims, ranks, fn->data());
     }
     const bool done = std::fabs(new_fit - cur_fit) < cfg.fit_tol;            // tucker.py:389
     std::swap(cc, cn);

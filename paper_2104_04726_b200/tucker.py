@@ -201,35 +201,91 @@ def fit(t: DenseTensor, model: TuckerModel, method: str = "core") -> float:
 # ---------------------------------------------------------------------------
 
 
-@dataclass
 class PPState:
-    anchors: list[np.ndarray]
-    deltas: list[np.ndarray]
-    op_single: list[DenseTensor]
-    op_pair: dict[tuple[int, int], DenseTensor]
-    contraction_count: int
+    """Anchor factors, their drift and the skip-one / skip-two operators
+    (tucker.py:199-219), held by libtmb's native ``tmb_pp`` handle on the
+    device. ``op_single`` / ``op_pair`` are host views fetched on first access;
+    ``deltas`` may be assigned as in the reference (it is uploaded before the
+    next ``pp_sweep``)."""
+
+    def __init__(self, handle, dims, ranks, anchors, count: int):
+        self._h = L.C.c_void_p(handle)
+        self._dims = tuple(dims)
+        self._ranks = tuple(ranks)
+        self.anchors = [np.asarray(a, dtype=np.float64) for a in anchors]
+        self._deltas = [np.zeros_like(a) for a in self.anchors]
+        self._dirty = False          # host deltas newer than the device copy
+        self._max_rel = 0.0
+        self.contraction_count = int(count)
+        self._single = None
+        self._pair = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            L.LIB.tmb_pp_destroy(h)
+
+    def _op(self, mask: int) -> DenseTensor:
+        d = (L.C.c_int64 * len(self._dims))()
+        p = L.C.c_void_p()
+        if L.LIB.tmb_pp_operator(self._h, mask, L.C.byref(p), d) != L.TMB_OK:
+            raise RuntimeError(f"pp operator {mask} unavailable")
+        dims = tuple(int(v) for v in d)
+        out = L.empty_f64(int(np.prod(dims)))
+        h = L.ctx()
+        L.check(L.LIB.tmb_pp_operator_copy(h, self._h, mask, L.ptr(out)), h)
+        return DenseTensor(L.host_f(out, dims))
+
+    @property
+    def op_single(self) -> list[DenseTensor]:
+        if self._single is None:
+            self._single = [self._op(1 << n) for n in range(len(self._dims))]
+        return self._single
+
+    @property
+    def op_pair(self) -> dict[tuple[int, int], DenseTensor]:
+        if self._pair is None:
+            n_modes = len(self._dims)
+            self._pair = {(i, n): self._op((1 << i) | (1 << n)) for i in range(n_modes) for n in range(i + 1, n_modes)}
+        return self._pair
 
     def pair(self, i: int, n: int) -> DenseTensor:
         return self.op_pair[(i, n) if i < n else (n, i)]
 
+    @property
+    def deltas(self) -> list[np.ndarray]:
+        return self._deltas
+
+    @deltas.setter
+    def deltas(self, value) -> None:
+        self._deltas = [np.asarray(d, dtype=np.float64) for d in value]
+        self._dirty = True
+
+    def _upload(self, mats, are_factors: bool) -> float:
+        h = L.ctx()
+        dev = [L.dev_f64(m) for m in mats]
+        mr = L.C.c_double()
+        L.check(L.LIB.tmb_pp_set_deltas(h, self._h, L.ptrs(dev), 1 if are_factors else 0, L.C.byref(mr)), h)
+        return float(mr.value)
+
     def set_current(self, factors: Sequence[np.ndarray]) -> None:
-        self.deltas = [np.asarray(f, dtype=np.float64) - a for f, a in zip(factors, self.anchors)]
+        """deltas = factors - anchors, on the device (tucker.py:212-213)."""
+        self._max_rel = self._upload(factors, True)
+        self._deltas = [np.asarray(f, dtype=np.float64) - a for f, a in zip(factors, self.anchors)]
+        self._dirty = False
 
     def max_rel_delta(self) -> float:
-        out = 0.0
-        for d, a in zip(self.deltas, self.anchors):
-            out = max(out, _frob(d) / _frob(a))
-        return out
-
-
-def _frob(m: np.ndarray) -> float:
-    return fro_norm(DenseTensor(np.asarray(m, dtype=np.float64)))
+        """max_n ||d_n|| / ||a_n|| (tucker.py:215-219)."""
+        if self._dirty:
+            self._max_rel = self._upload(self._deltas, False)
+            self._dirty = False
+        return self._max_rel
 
 
 def pp_operators(t: DenseTensor, anchors: Sequence[np.ndarray]) -> PPState:
-    """Skip-one and skip-two contractions through a memoised dimension tree
-    whose parent re-adds the largest contracted mode (tucker.py:222-265), so
-    every node is an ascending contraction. Each node is one device TTM."""
+    """Skip-one and skip-two contractions through the memoised dimension tree
+    whose parent re-adds the largest contracted mode (tucker.py:222-265), built
+    natively in one call (``tmb_pp_operators``)."""
     n_modes = t.ndim
     if len(anchors) != n_modes:
         raise ValueError(f"expected {n_modes} anchors, got {len(anchors)}")
@@ -237,68 +293,37 @@ def pp_operators(t: DenseTensor, anchors: Sequence[np.ndarray]) -> PPState:
         a = np.asarray(a)
         if a.ndim != 2 or a.shape[0] != t.dims[n]:
             raise ValueError(f"mode {n}: anchor shape {a.shape} does not match dim {t.dims[n]}")
-    cache: dict[frozenset, DenseTensor] = {frozenset(range(n_modes)): t}
-    count = 0
-
-    def node(free: frozenset) -> DenseTensor:
-        nonlocal count
-        got = cache.get(free)
-        if got is not None:
-            return got
-        m = max(i for i in range(n_modes) if i not in free)
-        out = ttm(node(free | {m}), np.asarray(anchors[m], dtype=np.float64).T, m)
-        count += 1
-        cache[free] = out
-        return out
-
-    op_single = [node(frozenset((n,))) for n in range(n_modes)]
-    op_pair = {(i, n): node(frozenset((i, n))) for i in range(n_modes) for n in range(i + 1, n_modes)}
-    anchors64 = [np.asarray(a, dtype=np.float64) for a in anchors]
-    return PPState(anchors64, [np.zeros_like(a) for a in anchors64], op_single, op_pair, count)
-
-
-def _pp_operand(state: PPState, n: int) -> DenseTensor:
-    """First-order skip-n estimate (tucker.py:268-282); accumulation on the device."""
-    y = state.op_single[n]
-    acc_d = None
-    for i in range(len(state.anchors)):
-        if i == n:
-            continue
-        d = state.deltas[i]
-        if not np.any(d):
-            continue
-        corr = ttm(state.pair(i, n), d.T, i)
-        if acc_d is None:
-            acc_d = L.dev_f64(corr.array)
-        else:
-            h = L.ctx()
-            cd = L.dev_f64(corr.array)
-            L.check(L.LIB.tmb_axpy(h, corr.size, 1.0, L.ptr(cd), L.ptr(acc_d)), h)
-    if acc_d is None:
-        return y
+    ranks = tuple(int(np.asarray(a).shape[1]) for a in anchors)
     h = L.ctx()
-    yd = L.dev_f64(y.array)
-    L.check(L.LIB.tmb_axpy(h, y.size, 1.0, L.ptr(yd), L.ptr(acc_d)), h)
-    return DenseTensor(L.host_f(acc_d, y.dims))
+    x = L.dev_f64(t.array)
+    dev = [L.dev_f64(a) for a in anchors]
+    out = L.C.c_void_p()
+    L.check(L.LIB.tmb_pp_operators(h, L.ptr(x), L.F64, n_modes, L.i64s(t.dims), L.i64s(ranks), L.ptrs(dev),
+                                   L.C.byref(out)), h)
+    cnt = L.C.c_int()
+    L.LIB.tmb_pp_info(out, None, L.C.byref(cnt))
+    return PPState(out.value, t.dims, ranks, anchors, cnt.value)
 
 
 def pp_sweep(state: PPState, model: TuckerModel, return_operands: bool = False):
-    """One accelerated sweep from the precomputed operators (tucker.py:285-311)."""
-    ranks = model.ranks
-    factors = list(model.factors)
-    operands: list[DenseTensor] = []
-    last_y = None
-    for n in range(len(factors)):
-        y = _pp_operand(state, n)
-        if return_operands:
-            operands.append(y)
-        factors[n] = leading_eigvecs(gram(unfold(y, n)), ranks[n])[0]
-        last_y = y
-    n_last = len(factors) - 1
-    core = ttm(last_y, factors[n_last].T, n_last)
-    out = TuckerModel(core, factors, model.source_dims)
+    """One accelerated sweep from the precomputed operators and the entry
+    deltas (tucker.py:285-311), one native call (``tmb_pp_sweep``); the core is
+    the pp estimate Y_{N-1} x_{N-1} S_{N-1}^T, as in the reference."""
+    if state._dirty:
+        state.max_rel_delta()
+    dims, ranks = state._dims, tuple(model.ranks)
+    if ranks != state._ranks:
+        raise ValueError(f"model ranks {ranks} do not match the pp operators' {state._ranks}")
+    n_modes = len(dims)
+    h = L.ctx()
+    core = L.empty_f64(int(np.prod(ranks)))
+    facs = [L.empty_f64(s * r) for s, r in zip(dims, ranks)]
+    op_dims = [tuple(dims[m] if m == n else ranks[m] for m in range(n_modes)) for n in range(n_modes)]
+    ops = [L.empty_f64(int(np.prod(d))) for d in op_dims] if return_operands else None
+    L.check(L.LIB.tmb_pp_sweep(h, state._h, L.ptr(core), L.ptrs(facs), L.ptrs(ops) if ops else None), h)
+    out = _model_from_dev(core, facs, ranks, model.source_dims)
     if return_operands:
-        return out, operands
+        return out, [DenseTensor(L.host_f(o, d)) for o, d in zip(ops, op_dims)]
     return out
 
 

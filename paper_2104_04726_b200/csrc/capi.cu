@@ -483,10 +483,8 @@ int tmb_encode_stack_u8(tmb_ctx* ctx, const uint8_t* rgb, int64_t n_img, int64_t
     tmb::absmax_async(c, core, Pc, sc);
     tmb::quant_step(c, sc, qp, sc + 1);
     tmb::quantize(c, core, Pc, sc + 1, levels);
-    if (rel_err_host) {
-      double* rec = tmb::alloc<double>(c, (size_t)P);
-      tmb::reconstruct_dev(c, r, d, core, factors, rec);
-      tmb::resid2_async(c, tensor, tmb::F32, rec, P, sc + 2);
+    if (rel_err_host) {  // K9: reconstruction fused with the residual norm (nothing written)
+      tmb::reconstruct_resid_dev(c, r, d, core, factors, tensor, tmb::F32, sc + 2);
       tmb::sumsq_async(c, tensor, tmb::F32, P, sc + 3);
     }
     TMB_CUDA(cudaMemcpyAsync(c.host_pinned, sc, sizeof(double) * 4, cudaMemcpyDeviceToHost, c.stream));

@@ -134,6 +134,74 @@ __global__ void __launch_bounds__(ST2_THREADS) k_small_ttm2(const T* __restrict_
   }
 }
 
+// K9 fused epilogue: the last two (small) mode products of the reconstruction
+// with the residual against the source tensor, sum (t - y)^2, instead of
+// writing y. Same products, in the same order, as k_small_ttm2; the squared
+// differences reduce per block (fixed order) into part[blockIdx.x].
+template <typename TT>
+__global__ void __launch_bounds__(ST2_THREADS) k_small_ttm2_resid(const double* __restrict__ x, int64_t L, int K1,
+                                                                  int K2, int64_t Rr, const double* __restrict__ m1,
+                                                                  int r1, int64_t s1r, int64_t s1k,
+                                                                  const double* __restrict__ m2, int r2, int64_t s2r,
+                                                                  int64_t s2k, const TT* __restrict__ t,
+                                                                  double* __restrict__ part) {
+  extern __shared__ double sm2[];
+  __shared__ double red[ST2_THREADS / 32];
+  double* A1 = sm2;
+  double* A2 = A1 + K1 * r1;
+  double* tb = A2 + K2 * r2;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < K1 * r1; e += blockDim.x) A1[e] = m1[(e % r1) * s1r + (e / r1) * s1k];
+  for (int e = tid; e < K2 * r2; e += blockDim.x) A2[e] = m2[(e % r2) * s2r + (e / r2) * s2k];
+  __syncthreads();
+  double ss = 0.0;
+  const int64_t total = L * Rr;
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + tid; f < total; f += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = f % L, rr = f / L;
+    const double* xp = x + l + L * (int64_t)K1 * K2 * rr;
+    for (int k2 = 0; k2 < K2; ++k2) {
+      double acc[ST2_R1];
+#pragma unroll
+      for (int i = 0; i < ST2_R1; ++i) acc[i] = 0.0;
+      for (int k1 = 0; k1 < K1; ++k1) {
+        const double xv = xp[L * (k1 + (int64_t)K1 * k2)];
+#pragma unroll
+        for (int i = 0; i < ST2_R1; ++i)
+          if (i < r1) acc[i] = fma(A1[k1 * r1 + i], xv, acc[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < ST2_R1; ++i)
+        if (i < r1) tb[(k2 * r1 + i) * ST2_THREADS + tid] = acc[i];
+    }
+    const TT* tp = t + l + L * (int64_t)r1 * r2 * rr;
+    for (int i2 = 0; i2 < r2; ++i2) {
+      double acc[ST2_R1];
+#pragma unroll
+      for (int i = 0; i < ST2_R1; ++i) acc[i] = 0.0;
+      for (int k2 = 0; k2 < K2; ++k2) {
+        const double a = A2[k2 * r2 + i2];
+#pragma unroll
+        for (int i = 0; i < ST2_R1; ++i)
+          if (i < r1) acc[i] = fma(a, tb[(k2 * r1 + i) * ST2_THREADS + tid], acc[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < ST2_R1; ++i)
+        if (i < r1) {
+          const double d = (double)tp[L * (i + (int64_t)r1 * i2)] - acc[i];
+          ss = fma(d, d, ss);
+        }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((tid & 31) == 0) red[tid >> 5] = ss;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < ST2_THREADS / 32; ++w) s += red[w];
+    part[blockIdx.x] = s;
+  }
+}
+
 // ---- small-mode Gram, pass 1: per-block partial upper-triangle sums.
 constexpr int SG_THREADS = 256, SG_MAXPP = 9;  // K <= 64 -> 2080 pairs <= 9*256
 template <typename T>
@@ -418,6 +486,30 @@ bool small_ttm2(Ctx& c, const void* x, DType tx, int64_t L, int64_t K1, int64_t 
     k_small_ttm2<double><<<blocks, ST2_THREADS, smem, c.stream>>>((const double*)x, L, (int)K1, (int)K2, Rr, m1,
                                                                    (int)r1, s1r, s1k, m2, (int)r2, s2r, s2k, y);
   LAUNCHED("k_small_ttm2");
+  return true;
+}
+
+bool small_ttm2_resid(Ctx& c, const double* x, int64_t L, int64_t K1, int64_t K2, int64_t Rr, const double* m1,
+                      int64_t r1, int64_t s1r, int64_t s1k, const double* m2, int64_t r2, int64_t s2r, int64_t s2k,
+                      const void* t, DType tt, double* out_dev) {
+  if (r1 > ST2_R1 || K2 * r1 > ST2_T || K1 > 64 || K2 > 64 || r2 > 64) return false;
+  const int64_t total = L * Rr;
+  const size_t smem = sizeof(double) * (K1 * r1 + K2 * r2 + (size_t)K2 * r1 * ST2_THREADS);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, ST2_THREADS), 8LL * c.num_sms));
+  const void* fn = tt == F32 ? (const void*)k_small_ttm2_resid<float> : (const void*)k_small_ttm2_resid<double>;
+  set_smem_attr(c, fn, sizeof(double) * (64 * 8 + 64 * 64 + (size_t)ST2_T * ST2_THREADS));
+  double* part = alloc<double>(c, (size_t)blocks);
+  if (tt == F32)
+    k_small_ttm2_resid<float><<<blocks, ST2_THREADS, smem, c.stream>>>(x, L, (int)K1, (int)K2, Rr, m1, (int)r1, s1r,
+                                                                        s1k, m2, (int)r2, s2r, s2k,
+                                                                        (const float*)t, part);
+  else
+    k_small_ttm2_resid<double><<<blocks, ST2_THREADS, smem, c.stream>>>(x, L, (int)K1, (int)K2, Rr, m1, (int)r1,
+                                                                         s1r, s1k, m2, (int)r2, s2r, s2k,
+                                                                         (const double*)t, part);
+  LAUNCHED("k_small_ttm2_resid");
+  k_sum_final<<<1, 1024, 0, c.stream>>>(part, blocks, out_dev);
+  LAUNCHED("k_sum_final");
   return true;
 }
 

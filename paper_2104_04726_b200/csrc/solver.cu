@@ -346,6 +346,38 @@ void reconstruct_dev(Ctx& c, const Dims& ranks, const Dims& dims, const double* 
   (void)N;
 }
 
+// ||t - reconstruct(model)||^2 (tucker.py:166-171, fit(method="residual")
+// tucker.py:186-188) with the K9 fused epilogue: modes 0..N-3 as in
+// reconstruct_dev (ascending), then the last two small-mode products and the
+// residual in one pass, so the full reconstruction is never written.
+void reconstruct_resid_dev(Ctx& c, const Dims& ranks, const Dims& dims, const double* core,
+                           const double* const* factors, const void* t, DType tt, double* sse_dev) {
+  const int N = (int)dims.size();
+  const size_t mk = c.arena.mark();
+  bool fused = false;
+  if (N >= 3) {
+    Dims cur = ranks;
+    const double* src = core;
+    for (int n = 0; n < N - 2; ++n) {
+      Dims nd = cur;
+      nd[n] = dims[n];
+      double* dst = alloc<double>(c, (size_t)prod(nd, 0, N));
+      ttm_dev(c, src, F64, cur, n, factors[n], dims[n], 1, dims[n], dst);  // y = x x_n S_n (S_n: dims x ranks)
+      src = dst;
+      cur = nd;
+    }
+    const int a = N - 2, b = N - 1;
+    fused = small_ttm2_resid(c, src, prod(cur, 0, a), ranks[a], ranks[b], 1, factors[a], dims[a], 1, dims[a],
+                             factors[b], dims[b], 1, dims[b], t, tt, sse_dev);
+  }
+  if (!fused) {
+    double* rec = alloc<double>(c, (size_t)prod(dims, 0, N));
+    reconstruct_dev(c, ranks, dims, core, factors, rec);
+    resid2_async(c, t, tt, rec, prod(dims, 0, N), sse_dev);
+  }
+  c.arena.release(mk);
+}
+
 // ------------------------------------------------------------------ pairwise perturbation
 // tucker.py:199-311. Operators persist across sweeps (own cudaMalloc buffers,
 // outside the per-sweep arena); rebuilt only when the PP phase refreshes.

@@ -20,6 +20,8 @@ void hooi_sweep_dev(Ctx& c, const void* x, DType tx, const Dims& dims, const Dim
                     const double* const* fin, bool greedy, double* core, double* const* fout);
 void reconstruct_dev(Ctx& c, const Dims& ranks, const Dims& dims, const double* core, const double* const* factors,
                      double* out);
+void reconstruct_resid_dev(Ctx& c, const Dims& ranks, const Dims& dims, const double* core,
+                           const double* const* factors, const void* t, DType tt, double* sse_dev);
 // pairwise-perturbation operators (tucker.py:199-311): device buffers that outlive the arena
 struct DevBuf {
   double* p = nullptr;

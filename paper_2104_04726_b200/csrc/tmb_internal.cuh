@@ -128,6 +128,11 @@ void small_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t Rr
 bool small_ttm2(Ctx& c, const void* x, DType tx, int64_t L, int64_t K1, int64_t K2, int64_t Rr, const double* m1,
                 int64_t r1, int64_t s1r, int64_t s1k, const double* m2, int64_t r2, int64_t s2r, int64_t s2k,
                 double* y);
+// the same two products fused with sum (t - y)^2 (K9 epilogue: y is never written);
+// false (nothing launched) outside small_ttm2's limits
+bool small_ttm2_resid(Ctx& c, const double* x, int64_t L, int64_t K1, int64_t K2, int64_t Rr, const double* m1,
+                      int64_t r1, int64_t s1r, int64_t s1k, const double* m2, int64_t r2, int64_t s2r, int64_t s2k,
+                      const void* t, DType tt, double* out_dev);
 void small_gram(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t Rr, double* g);
 double sumsq(Ctx& c, const void* x, DType tx, int64_t n);           // sync D2H
 void sumsq_async(Ctx& c, const void* x, DType tx, int64_t n, double* out_dev);

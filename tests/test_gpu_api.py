@@ -482,6 +482,14 @@ def test_colour_u8_exhaustive(space):
     fn = oracle.rgb_to_ycbcr if space == "ycbcr" else oracle.rgb_to_ipt
     ref = fn(u8.reshape(4096, 4096, 3).astype(np.float64) / 255.0).astype(np.float32)
     assert np.array_equal(got, ref), int((got != ref).sum())
+    # ... and against the REFERENCE's own colour on the same 2^24 triples (sha256 of its
+    # fp32-rounded output, scripts/make_golden_colour_exhaustive.py)
+    import hashlib
+    import json
+    from conftest import GOLDEN
+
+    want = json.loads((GOLDEN / "colour_exhaustive.json").read_text())[space]
+    assert hashlib.sha256(np.ascontiguousarray(got).tobytes()).hexdigest() == want
     rng = np.random.default_rng(21)
     imgs = rng.integers(0, 256, size=(1, 2, 37, 70, 3), dtype=np.uint8)
     got2 = tb.coding_tensor(imgs, space).cpu().numpy().reshape((37, 70, 3, 2), order="F")

@@ -62,6 +62,57 @@ __device__ __forceinline__ double spow043(double v) {
   return v > 0.0 ? a : (v < 0.0 ? -a : 0.0);
 }
 
+// |v|^0.43 for the u8 IPT path from 128-entry tables + short polynomials, all
+// fp64 (~20 DFMA-class ops instead of the ~70 of CUDA's log2 + exp2):
+//   log2 a = e + lc_j + log2(1 + r) for a = m 2^e, r = m invc_j - 1 (|r| < 2^-8),
+//            lc_j = -log2(invc_j), j = the top 7 bits of m,
+//            log2(1 + r) by its degree-6 Taylor polynomial (truncation < 2^-56 |r|);
+//   2^z    = 2^k 2^(i/128) e^(g ln 2), z = k + i/128 + g, g < 2^-7, degree-6 polynomial.
+// Error ~2e-15 relative (the same class as exp2(0.43 log2)); the fp32 outputs are
+// checked bit-identical to the reference on all 2^24 u8 triples
+// (tests/test_gpu_api.py::test_colour_u8_exhaustive). The tables are staged in
+// shared memory by the kernel.
+constexpr int PT = 128;
+struct PowTab {
+  double invc[PT];   // RN(1 / (1 + (j + 0.5) / 128))
+  double lc[PT];     // -log2(invc[j]) (so log2 m = lc + log2(m invc) exactly in real arithmetic)
+  double e2[PT];     // 2^(j / 128)
+};
+__device__ PowTab g_powtab;
+
+__device__ __forceinline__ double pow043_tab(double v, const double* invc, const double* lc, const double* e2) {
+  const double a = fabs(v);
+  const long long bits = __double_as_longlong(a);
+  const int eb = (int)(bits >> 52);
+  if (a == 0.0 || eb == 0) return a == 0.0 ? 0.0 : (v > 0.0 ? 1.0 : -1.0) * exp2(0.43 * log2(a));  // zero / subnormal
+  const int j = (int)((bits >> 45) & (PT - 1));
+  const double m = __longlong_as_double((bits & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
+  const double r = fma(m, invc[j], -1.0);
+  // log2(1 + r) = r (a1 + r (a2 + ... + r a6)), a_k = (-1)^(k+1) / (k ln 2)
+  double p = -0.24044917348149390;                 // -1/(6 ln2)
+  p = fma(p, r, 0.28853900817779268);              // 1/(5 ln2)
+  p = fma(p, r, -0.36067376022224085);             // -1/(4 ln2)
+  p = fma(p, r, 0.48089834696298783);              // 1/(3 ln2)
+  p = fma(p, r, -0.72134752044448170);             // -1/(2 ln2)
+  p = fma(p, r, 1.4426950408889634);               // 1/ln2
+  const double lg = ((double)(eb - 1023) + lc[j]) + p * r;
+  const double z = 0.43 * lg;                      // in (-8, 0] for a in (2^-18, 1]; any sign works
+  const double kf = floor(z);
+  const double f = z - kf;                         // exact, in [0, 1)
+  const double fi = floor(f * (double)PT);
+  const double g = f - fi * (1.0 / PT);            // exact, in [0, 1/128)
+  const double t = g * 0.69314718055994531;
+  double q = 1.0 / 720.0;
+  q = fma(q, t, 1.0 / 120.0);
+  q = fma(q, t, 1.0 / 24.0);
+  q = fma(q, t, 1.0 / 6.0);
+  q = fma(q, t, 0.5);
+  q = fma(q, t, 1.0);
+  q = fma(q, t, 1.0);
+  const double y = e2[(int)fi] * q * __longlong_as_double((long long)(1023 + (int)kf) << 52);
+  return v > 0.0 ? y : -y;
+}
+
 __device__ __forceinline__ void ipt_from_lin(const double* lin, double* o) {
   // color.py:150-158
   double xyz[3], lms[3], lmsp[3], ipt[3];
@@ -127,11 +178,16 @@ __global__ void __launch_bounds__(256) k_color_u8(const uint8_t* __restrict__ rg
   __shared__ __align__(16) uint8_t su8[CT_H][CT_ROWB];  // 4-byte aligned rows
   __shared__ __align__(16) float so[3][CT_W][CT_FP];
   __shared__ double lut[256];
+  __shared__ double ptab[SPACE == TMB_SPACE_IPT ? 3 * PT : 1];
   const int t = threadIdx.x;
   const int64_t img = blockIdx.z;
   const int64_t x0 = (int64_t)blockIdx.x * CT_W, y0 = (int64_t)blockIdx.y * CT_H;
   const bool full = (x0 + CT_W <= w) && (y0 + CT_H <= h);
-  if (space == TMB_SPACE_IPT) lut[t] = g_eotf[t];
+  if (space == TMB_SPACE_IPT) {
+    lut[t] = g_eotf[t];
+    const double* gp = g_powtab.invc;  // invc | lc | e2, contiguous
+    for (int i = t; i < 3 * PT; i += 256) ptab[i] = gp[i];
+  }
   else if (space != TMB_SPACE_YCBCR) lut[t] = __ddiv_rn((double)t, 255.0);
   const uint8_t* src = rgb + (img * h + y0) * w * 3 + x0 * 3;
   if (full && (w & 15) == 0 && ((reinterpret_cast<uintptr_t>(rgb) & 15) == 0)) {
@@ -184,7 +240,8 @@ __global__ void __launch_bounds__(256) k_color_u8(const uint8_t* __restrict__ rg
         double lmsp[3];
 #pragma unroll
         for (int i = 0; i < 3; ++i)
-          lmsp[i] = spow043(fma(l2, cc.lin2lms[3 * i + 2], fma(l1, cc.lin2lms[3 * i + 1], l0 * cc.lin2lms[3 * i])));
+          lmsp[i] = pow043_tab(fma(l2, cc.lin2lms[3 * i + 2], fma(l1, cc.lin2lms[3 * i + 1], l0 * cc.lin2lms[3 * i])),
+                               ptab, ptab + PT, ptab + 2 * PT);
         double ipt[3];
 #pragma unroll
         for (int i = 0; i < 3; ++i)
@@ -457,6 +514,13 @@ void ensure_constants(Ctx& c) {
                               h.xyz2lms[3 * r + 2] * h.rgb2xyz[6 + k2];
   TMB_CUDA(cudaMemcpyToSymbol(cc, &h, sizeof(h)));
   TMB_CUDA(cudaMemcpyToSymbol(g_eotf, h.eotf, sizeof(h.eotf)));
+  PowTab pt;
+  for (int j = 0; j < PT; ++j) {
+    pt.invc[j] = (double)(1.0L / (1.0L + ((long double)j + 0.5L) / PT));
+    pt.lc[j] = (double)(-std::log2((long double)pt.invc[j]));
+    pt.e2[j] = (double)std::exp2((long double)j / PT);
+  }
+  TMB_CUDA(cudaMemcpyToSymbol(g_powtab, &pt, sizeof(pt)));
   if (c.device >= 0 && c.device < 64) g_const_ready[c.device] = true;
 }
 

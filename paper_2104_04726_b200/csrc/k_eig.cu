@@ -1069,13 +1069,12 @@ static double orthonormalize(Ctx& c, double* x, int64_t n, int64_t k, double lim
   double e = e0;
   double* cur = x;
   double* nxt = y;
-  for (int it = 0; e >= kOrthoDone; ++it) {
+  for (int it = 0; e >= kOrthoDone; ++it) {  // w holds cur^T cur on entry to every iteration
     if (it >= 12) {
       c.arena.release(mk);
       throw Error(TMB_ENUMERIC, "leading_eigvecs: orthonormalisation did not converge, max|X^T X - I| = " +
                                     std::to_string(e));
     }
-    if (it > 0) form_xtx(c, cur, n, k, w);
     scale_identity_combo(c, w, k, 1.5, -0.5, b);
     GemmDesc g;
     g.M = n; g.N = k; g.K1 = k; g.K2 = 1;

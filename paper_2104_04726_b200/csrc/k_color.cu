@@ -25,6 +25,8 @@ struct ColorConst {
   double lms2xyz[9];
   double ipt2lms[9];
   double lin2lms[9];  // xyz2lms . rgb2xyz, for the u8 fast path
+  double plog[6];     // log2(1 + r) = r (plog[5] + r (plog[4] + ... + r plog[0]))
+  double pexp[7];     // 0.43, ln 2, then e^t coefficients 1/720 .. 1/2
 };
 __constant__ ColorConst cc;
 
@@ -80,33 +82,37 @@ struct PowTab {
 };
 __device__ PowTab g_powtab;
 
+__device__ __noinline__ double pow043_slow(double v) {  // zero / subnormal |v| (never on u8 inputs)
+  const double a = fabs(v);
+  if (a == 0.0) return 0.0;
+  const double y = exp2(0.43 * log2(a));
+  return v > 0.0 ? y : -y;
+}
+
 __device__ __forceinline__ double pow043_tab(double v, const double* invc, const double* lc, const double* e2) {
+  // polynomial coefficients and other fp64 constants come from the constant bank
+  // (cc.*): as immediates each use re-materialised a 64-bit value through two
+  // uniform-register moves per pixel
   const double a = fabs(v);
   const long long bits = __double_as_longlong(a);
   const int eb = (int)(bits >> 52);
-  if (a == 0.0 || eb == 0) return a == 0.0 ? 0.0 : (v > 0.0 ? 1.0 : -1.0) * exp2(0.43 * log2(a));  // zero / subnormal
+  if (eb == 0) return pow043_slow(v);  // zero / subnormal
   const int j = (int)((bits >> 45) & (PT - 1));
   const double m = __longlong_as_double((bits & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
   const double r = fma(m, invc[j], -1.0);
-  // log2(1 + r) = r (a1 + r (a2 + ... + r a6)), a_k = (-1)^(k+1) / (k ln 2)
-  double p = -0.24044917348149390;                 // -1/(6 ln2)
-  p = fma(p, r, 0.28853900817779268);              // 1/(5 ln2)
-  p = fma(p, r, -0.36067376022224085);             // -1/(4 ln2)
-  p = fma(p, r, 0.48089834696298783);              // 1/(3 ln2)
-  p = fma(p, r, -0.72134752044448170);             // -1/(2 ln2)
-  p = fma(p, r, 1.4426950408889634);               // 1/ln2
+  double p = cc.plog[0];
+#pragma unroll
+  for (int i = 1; i < 6; ++i) p = fma(p, r, cc.plog[i]);
   const double lg = ((double)(eb - 1023) + lc[j]) + p * r;
-  const double z = 0.43 * lg;                      // in (-8, 0] for a in (2^-18, 1]; any sign works
+  const double z = cc.pexp[0] * lg;                 // 0.43 log2 a
   const double kf = floor(z);
-  const double f = z - kf;                         // exact, in [0, 1)
+  const double f = z - kf;                          // exact, in [0, 1)
   const double fi = floor(f * (double)PT);
-  const double g = f - fi * (1.0 / PT);            // exact, in [0, 1/128)
-  const double t = g * 0.69314718055994531;
-  double q = 1.0 / 720.0;
-  q = fma(q, t, 1.0 / 120.0);
-  q = fma(q, t, 1.0 / 24.0);
-  q = fma(q, t, 1.0 / 6.0);
-  q = fma(q, t, 0.5);
+  const double g = fma(fi, -1.0 / PT, f);           // exact, in [0, 1/128)
+  const double t = g * cc.pexp[1];                  // g ln 2
+  double q = cc.pexp[2];
+#pragma unroll
+  for (int i = 3; i < 7; ++i) q = fma(q, t, cc.pexp[i]);
   q = fma(q, t, 1.0);
   q = fma(q, t, 1.0);
   const double y = e2[(int)fi] * q * __longlong_as_double((long long)(1023 + (int)kf) << 52);
@@ -512,8 +518,18 @@ void ensure_constants(Ctx& c) {
     for (int k2 = 0; k2 < 3; ++k2)
       h.lin2lms[3 * r + k2] = h.xyz2lms[3 * r] * h.rgb2xyz[k2] + h.xyz2lms[3 * r + 1] * h.rgb2xyz[3 + k2] +
                               h.xyz2lms[3 * r + 2] * h.rgb2xyz[6 + k2];
-  TMB_CUDA(cudaMemcpyToSymbol(cc, &h, sizeof(h)));
   TMB_CUDA(cudaMemcpyToSymbol(g_eotf, h.eotf, sizeof(h.eotf)));
+  // log2(1 + r) Taylor coefficients (-1)^(k+1) / (k ln 2), k = 6 .. 1; e^t: 1/720 .. 1/2 (+ 1, 1 inline)
+  const long double ln2 = 0.693147180559945309417232121458176568L;
+  for (int k = 6; k >= 1; --k) h.plog[6 - k] = (double)(((k % 2) ? 1.0L : -1.0L) / ((long double)k * ln2));
+  h.pexp[0] = 0.43;
+  h.pexp[1] = (double)ln2;
+  h.pexp[2] = (double)(1.0L / 720.0L);
+  h.pexp[3] = (double)(1.0L / 120.0L);
+  h.pexp[4] = (double)(1.0L / 24.0L);
+  h.pexp[5] = (double)(1.0L / 6.0L);
+  h.pexp[6] = 0.5;
+  TMB_CUDA(cudaMemcpyToSymbol(cc, &h, sizeof(h)));
   PowTab pt;
   for (int j = 0; j < PT; ++j) {
     pt.invc[j] = (double)(1.0L / (1.0L + ((long double)j + 0.5L) / PT));

@@ -126,3 +126,37 @@ def test_encode_stream_errors(golden):
     bad = scene.map_images(lambda im: tb.ColorImage(np.where(im.pixels > 0.5, np.nan, im.pixels)))
     with pytest.raises(ValueError, match="finite"):
         tb.encode_stream(bad, tb.EncodeConfig(preset=1))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["default_ycbcr", "exact_ipt"])
+def test_reference_decodes_our_stream(golden, name):
+    """The REFERENCE's decode_stream (oracle/_ref, installed unmodified) reads the
+    bytes our encode_stream writes, and decodes them to the PSNR our
+    decode_stream reports: the stream format is the reference's."""
+    import sys
+    from pathlib import Path
+
+    ref_dir = Path(__file__).resolve().parents[1] / "oracle" / "_ref"
+    if not (ref_dir / "tmcodec").exists():
+        pytest.fail("oracle/_ref is not built (python oracle/build_ref.py)")
+    sys.path.insert(0, str(ref_dir))
+    try:
+        import tmcodec as ref
+        assert str(Path(ref.__file__).resolve()).startswith(str(ref_dir))
+    finally:
+        sys.path.remove(str(ref_dir))
+    z = golden("stream")
+    images = z[f"{name}_images"]
+    kw = {"default_ycbcr": dict(space="ycbcr", preset=2, qp=30),
+          "exact_ipt": dict(space="ipt", ranks=(12, 16, 3, 2), qp=20, entropy_tag=0, max_sweeps=6, fit_tol=1e-300,
+                            pp_enter_tol=0.0)}[name]
+    scene = _scene(images)
+    data = tb.serialize_stream(tb.encode_stream(scene, tb.EncodeConfig(**kw)))
+    ours = tb.scene_psnr(scene, tb.decode_stream(tb.parse_stream(data)))
+    v_, e_, h, w, _ = images.shape
+    rscene = ref.SceneStack("golden", v_, e_, w, h, "rgb",
+                            {(v, e): ref.ColorImage(images[v, e].astype(np.float64) / 255.0)
+                             for v in range(v_) for e in range(e_)})
+    theirs = ref.scene_psnr(rscene, ref.decode_stream(ref.parse_stream(data)))
+    assert abs(ours.left - theirs.left) < 1e-9 and abs(ours.right - theirs.right) < 1e-9

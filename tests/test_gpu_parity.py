@@ -257,3 +257,22 @@ def test_ozaki_tcgen05_ttm_matches_fp64():
     scale = torch.einsum("lcji,jr->lcri", x.double().view(8, 3, 1024, 512).abs(), u.abs())
     assert (err.abs() / scale).max().item() < 4e-15
     assert (err.norm() / ref.norm()).item() < 4e-15
+
+
+def test_encode_stacks_batch_equals_per_stack():
+    """The batched data-parallel unit (encode_stacks: H2D of stack i+1 on a copy
+    stream overlapping the solve of stack i) returns, stack by stack, exactly
+    what encode_stack returns for that stack alone."""
+    import torch
+
+    cfg = CONFIGS["c3"]
+    stacks = [make_stack(cfg, seed=s, frame=s, height=270, width=480) for s in range(3)]
+    ranks = (34, 60, 3, 5)
+    pinned = [torch.from_numpy(s).pin_memory() for s in stacks]
+    batch = tb.encode_stacks(pinned, cfg.space, ranks, 4, cfg.qp)
+    assert len(batch) == 3
+    for s, r in zip(stacks, batch):
+        one = tb.encode_stack(s, cfg.space, ranks, 4, cfg.qp)
+        assert np.array_equal(r.levels, one.levels) and r.step == one.step
+        assert r.rel_err == one.rel_err
+        assert [x.fit for x in r.trace.records] == [x.fit for x in one.trace.records]

@@ -177,7 +177,14 @@ def solve_channels(images_u8, space: str, ranks: Sequence[int], cfg, qp: int | N
     is converted straight into three (H, W, E, V) float32 tensors
     (stack_to_tensor, sceneio.py:191-199) and each is solved with ``cfg``
     (a SolveConfig whose ranks are the (H, W, E, V) ranks). Returns a list of
-    (TuckerModel, SolveTrace), or of QuantizedModel when ``qp`` is given."""
+    (TuckerModel, SolveTrace), or of QuantizedModel when ``qp`` is given.
+
+    Precision note: this is the BASELINE harness's format -- the u8 colour
+    kernel writes fp32(reference float64 colour), bit for bit, and the solve
+    accumulates in fp64 from those fp32 values. The reference codec solves the
+    float64 colour values themselves; the float64 drop-in for that is
+    ``encode_stream`` / ``solve_channels_f64`` (App. B.1(ii) measures the
+    difference: angles ~1e-4 rad, levels equal except ties)."""
     from .tucker import solve_device
 
     torch = L._torch()

@@ -1047,7 +1047,10 @@ static double offidentity_host(Ctx& c, const double* w, int64_t k, double* chk) 
 
 // Above this max|X^T X - I| the vectors are not a small perturbation of an
 // orthonormal eigenbasis: a cluster was resolved as (nearly) parallel vectors.
-constexpr double kRepairOrtho = 1e-2;  // C2 solves measure up to 2e-4 (TMB_EIG_STATS)
+// NS handles anything below 0.5 (as in round 1; C2 solves measure up to 2e-4 with
+// TMB_EIG_STATS, C4 at ranks (1080, 1920): n = 3840 up to 1.6e-2): the repair is for
+// (nearly) parallel vectors only
+constexpr double kRepairOrtho = 0.5;
 constexpr double kOrthoDone = 1e-13;
 
 // Newton-Schulz: X <- X (1.5 I - 0.5 X^T X), quadratically convergent from the
@@ -1135,9 +1138,35 @@ static void repair_clusters(Ctx& c, const double* d, const double* e, int64_t n,
       LAUNCHED("k_fill_rand");
       const size_t sm = sizeof(double) * (size_t)m;
       set_smem_attr(c, (const void*)k_cgs2, std::max<size_t>(sm, 48 * 1024));
-      for (int it = 0; it < 3; ++it) {  // the cluster dominates (T - sigma)^-1 by gap/spread per step
+      // the other k - m vectors with the cluster's columns zeroed: each step projects them out
+      // of Y (twice, classical Gram-Schmidt by two GEMMs), so the repaired basis cannot drift
+      // towards eigenvectors outside the cluster
+      double* qo = alloc<double>(c, (size_t)n * k);
+      double* cm = alloc<double>(c, (size_t)k * m);
+      copy_d(c, qo, z, n * k);
+      TMB_CUDA(cudaMemsetAsync(qo + a * n, 0, sizeof(double) * n * m, c.stream));
+      auto project_out = [&]() {
+        GemmDesc g1;  // C = Qo^T Y  (k x m)
+        g1.M = k; g1.N = m; g1.K1 = n;
+        g1.A = qo; g1.sAm = n; g1.sAk1 = 1;
+        g1.B = ya; g1.sBk1 = 1; g1.sBn = n;
+        g1.C = cm; g1.sCm = 1; g1.sCn = k;
+        gemm(c, g1);
+        GemmDesc g2;  // Y -= Qo C
+        g2.M = n; g2.N = m; g2.K1 = k;
+        g2.A = qo; g2.sAm = 1; g2.sAk1 = n;
+        g2.B = cm; g2.sBk1 = 1; g2.sBn = k;
+        g2.C = ya; g2.sCm = 1; g2.sCn = n;
+        g2.alpha = -1.0; g2.beta = 1.0;
+        gemm(c, g2);
+      };
+      for (int it = 0; it < 4; ++it) {  // the cluster dominates (T - sigma)^-1 by gap/spread per step
         k_tri_shift_solve<<<(unsigned)ceil_div(m, 128), 128, 0, c.stream>>>(d, e, n, sigma, pert, ya, n, m, scr);
         LAUNCHED("k_tri_shift_solve");
+        k_cgs2<<<1, 1024, sm, c.stream>>>(ya, n, n, m, bad);
+        LAUNCHED("k_cgs2");
+        project_out();
+        project_out();
         k_cgs2<<<1, 1024, sm, c.stream>>>(ya, n, n, m, bad);
         LAUNCHED("k_cgs2");
       }

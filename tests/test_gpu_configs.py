@@ -123,3 +123,22 @@ def test_c5_full_size_matches_reference(golden):
     res = tb.encode_stack(images, cfg.space, cfg.ranks, int(z["sweeps"]), cfg.qp)
     _check(res, z, "", sketch_tol=1e-3, fit_tol=1e-9, rel_tol=1e-8, head_tol=1e-4)
     _levels(res, z, "", 1e-2)
+
+
+def test_c4_full_sweeps_every_rank():
+    """BASELINE config 4 with all 15 sweeps at each curve point (late sweeps of
+    the (1080, 1920) ranks take n = 3840 Grams whose twisted vectors need the
+    Newton-Schulz clean-up at 1.6e-2): trace length, monotone fit, orthonormal
+    factors, the fit identity, and the error-vs-rank curve decreasing."""
+    images = make_stack(CONFIGS["c4_8"], seed=0)
+    errs = []
+    for name in ("c4_8", "c4_4", "c4_2"):
+        cfg = CONFIGS[name]
+        res = tb.encode_stack(images, cfg.space, cfg.ranks, cfg.sweeps, 51)
+        res.model.validate()
+        fits = [r.fit for r in res.trace.records]
+        assert len(fits) == cfg.sweeps + 1
+        assert all(y >= x - 1e-12 for x, y in zip(fits, fits[1:]))
+        assert abs((1.0 - res.rel_err) - fits[-1]) < 1e-6
+        errs.append(res.rel_err)
+    assert errs[0] > errs[1] > errs[2]

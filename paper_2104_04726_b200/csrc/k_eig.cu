@@ -180,6 +180,7 @@ struct TrdArgs {
   double* part;  // 2 x gridDim
   int64_t k_end; // stop before step k_end (the cluster kernel continues from there)
   long long* prof;  // optional phase timestamps (TMB_TRD_PROFILE), else nullptr
+  int64_t k_begin = 0;  // first step (> 0 after the lazy panels: A holds the updated trailing block)
 };
 
 // Phase timestamps for 3 blocks x 8 sampled steps x 8 phases (diagnostics only).
@@ -308,30 +309,32 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) k_sytrd(const TrdArgs a) {
   double* A = a.A;
   const int nb = gridDim.x;
 
-  // ---- prologue: reflector 0 from the original column 0, then p_0 = tau_0 A22 v_0
-  for (int64_t i = tid; i < n; i += bd) vk[i] = (i >= 1) ? A[i] : 0.0;
+  // ---- prologue: reflector k0 from column k0 of the (updated) matrix, then
+  // p_k0 = tau A22 v_k0 (k0 = 0 for a whole solve, > 0 after the lazy panels)
+  const int64_t k0 = a.k_begin;
+  for (int64_t i = tid; i < n; i += bd) vk[i] = (i >= k0 + 1) ? A[i + n * k0] : 0.0;
   __syncthreads();
-  house(vk, 1, n, red, sc);
+  house(vk, k0 + 1, n, red, sc);
   double tau_k = sc[0];
   if (blockIdx.x == 0) {
-    if (tid == 0) { a.d[0] = A[0]; a.e[0] = sc[1]; a.tau[0] = tau_k; }
-    for (int64_t i = tid; i < n; i += bd) a.hv[i] = vk[i];
+    if (tid == 0) { a.d[k0] = A[k0 + n * k0]; a.e[k0] = sc[1]; a.tau[k0] = tau_k; }
+    for (int64_t i = tid; i < n; i += bd) a.hv[i + n * k0] = vk[i];
   }
   {
     double wpart = 0.0;
-    for (int64_t j = 1 + gw; j < n; j += GW) {
+    for (int64_t j = k0 + 1 + gw; j < n; j += GW) {
       double first[PASS_CH];
-      load_chunk(A + n * j, 1 + lane, n, first);
-      const double p = tau_k * column_pass(A + n * j, 1, n, lane, vk, vk, vk, 0.0, 0.0, false, first);
-      if (lane == 0) a.pbuf[j] = p;
+      load_chunk(A + n * j, k0 + 1 + lane, n, first);
+      const double p = tau_k * column_pass(A + n * j, k0 + 1, n, lane, vk, vk, vk, 0.0, 0.0, false, first);
+      if (lane == 0) a.pbuf[(k0 & 1) * n + j] = p;
       wpart = fma(p, vk[j], wpart);
     }
     const double s = block_sum_bcast(lane == 0 ? wpart : 0.0, red);
-    if (tid == 0) a.part[blockIdx.x] = s;
+    if (tid == 0) a.part[(k0 & 1) * nb + blockIdx.x] = s;
   }
   grid.sync();
 
-  for (int64_t k = 0; k + 2 < n && k < a.k_end; ++k) {
+  for (int64_t k = k0; k + 2 < n && k < a.k_end; ++k) {
     const int buf = (int)(k & 1);
     const double* pb = a.pbuf + buf * n;
     const double* pt = a.part + buf * nb;
@@ -433,6 +436,219 @@ __global__ void __launch_bounds__(TRD_THREADS, 2) k_sytrd(const TrdArgs a) {
     grid.sync();
     TRD_PROF(6);
   }
+}
+
+// ------------------------------------------------------------------ lazy (blocked) tridiagonalisation
+// For n whose Gram does not fit in L2 (C4/C5: n = 3840, 4320, 7680) the column
+// kernel streams the trailing matrix from HBM twice per step (read + write of the
+// rank-2 update). The lazy form (LAPACK's dlatrd, restated): within a panel of nb
+// steps starting at s, A keeps A_s and the updates live in V = [v_s ..], W = [w_s ..]:
+//   x   = A_s e_k - V (W^T e_k) - W (V^T e_k)           (column k of A_k)
+//   p   = tau (A_s v - V (W^T v) - W (V^T v)),  K = tau/2 p^T v,  w = p - K v,
+// so each step READS the trailing matrix once (the symv) and the panel's rank-2nb
+// update is applied by two DMMA GEMMs between panels (read + write once per nb
+// steps): ~(1 + 2/nb)/2 of the column kernel's HBM traffic. Two grid barriers per
+// step (after the symv + the V^T v / W^T v partials; after p + the K partials);
+// x and w are formed redundantly in every block (O(nb m) flops, V/W from L2).
+// The previous step's v, w stay in shared memory (vp, wp) and reach global V, W
+// one barrier later, so no step reads a V/W column written after its last barrier.
+// Read-only symv pass for the lazy kernel: dot of column col (rows >= lo) with v,
+// CHR rows per lane in flight (the stream is HBM-latency bound: more bytes in
+// flight per SM than the column kernel's update pass can afford in registers).
+template <int CHR>
+__device__ __forceinline__ double column_dot(const double* __restrict__ col, int64_t lo, int64_t n, int lane,
+                                             const double* __restrict__ v) {
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  double cur[CHR], nxt[CHR];
+  int64_t base = lo + lane;
+#pragma unroll
+  for (int u = 0; u < CHR; ++u) cur[u] = base + 32 * u < n ? col[base + 32 * u] : 0.0;
+  while (base < n) {
+    const int64_t nb = base + 32 * CHR;
+#pragma unroll
+    for (int u = 0; u < CHR; ++u) nxt[u] = nb + 32 * u < n ? col[nb + 32 * u] : 0.0;
+#pragma unroll
+    for (int u = 0; u < CHR; ++u) {
+      const int64_t i = base + 32 * u;
+      if (i < n) acc[u & 3] = fma(cur[u], v[i], acc[u & 3]);
+    }
+#pragma unroll
+    for (int u = 0; u < CHR; ++u) cur[u] = nxt[u];
+    base = nb;
+  }
+  return warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+}
+
+constexpr int LAZY_NB = 32;
+struct LazyArgs {
+  double* A; int64_t n; double* d; double* e; double* tau; double* hv;
+  double* VWV;                   // n x 3 LAZY_NB, ld n: [V | W | V] (the panel GEMM's A = [V W], B = [W V])
+  double* xbuf;                  // n: column k of A_k
+  double* praw; double* pfin;    // n each
+  double* part_s;                // gridDim x 2 LAZY_NB
+  double* part_k;                // gridDim
+  double* part_x;                // gridDim
+  int64_t s; int steps;
+};
+
+constexpr int LAZY_THREADS = 512;  // one block per SM (3n doubles of shared memory at n ~ 4k-8k)
+#ifndef TMB_LAZY_CH
+#define TMB_LAZY_CH 16
+#endif
+constexpr int LAZY_CH = TMB_LAZY_CH;  // symv rows per lane in flight
+__global__ void __launch_bounds__(LAZY_THREADS, 1) k_sytrd_lazy(const LazyArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sm[];
+  const int64_t n = a.n;
+  double* vp = sm;            // v of the previous step (then of this step)
+  double* wp = sm + n;        // w of the previous step (then of this step)
+  double* vn = sm + 2 * n;    // x, then this step's v
+  double* red = sm + 3 * n;   // 33
+  double* sc = red + 33;      // 8
+  double* vr = sc + 8;        // V[k, l'] (LAZY_NB)
+  double* wr = vr + LAZY_NB;  // W[k, l'] (LAZY_NB)
+  double* ss = wr + LAZY_NB;  // s1 (W^T v) | s2 (V^T v)   (2 LAZY_NB)
+  const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = bd >> 5;
+  const int NB = gridDim.x, b = blockIdx.x;
+  const int64_t gw = (int64_t)b * nw + warp, GW = (int64_t)NB * nw;
+  const double* A = a.A;
+  double* V = a.VWV;
+  double* W = a.VWV + n * LAZY_NB;
+  double* V2 = a.VWV + 2 * n * LAZY_NB;
+  for (int l = 0; l < a.steps; ++l) {
+    const int64_t k = a.s + l;
+    const int64_t m = n - k - 1, chunk = (m + NB - 1) / NB;
+    const int64_t r0 = k + 1 + (int64_t)b * chunk, r1 = r0 + chunk < n ? r0 + chunk : n;
+    // ---- x = column k of A_k over this block's row chunk (rows >= k+1), ||x||^2 partial
+    if (tid < l) {
+      vr[tid] = tid == l - 1 ? vp[k] : V[k + n * tid];
+      wr[tid] = tid == l - 1 ? wp[k] : W[k + n * tid];
+    }
+    __syncthreads();
+    double s2 = 0.0;
+    for (int64_t i = r0 + tid; i < r1; i += bd) {
+      double x = A[i + n * k];
+      for (int q = 0; q + 1 < l; ++q) x = x - V[i + n * q] * wr[q] - W[i + n * q] * vr[q];
+      if (l >= 1) x = x - vp[i] * wr[l - 1] - wp[i] * vr[l - 1];
+      a.xbuf[i] = x;
+      if (i >= k + 2) s2 = fma(x, x, s2);
+    }
+    const double xb = block_sum_all(s2, red);
+    if (tid == 0) a.part_x[b] = xb;
+    if (b == 0 && tid == 0) {
+      double dk = A[k + n * k];
+      for (int q = 0; q < l; ++q) dk = dk - vr[q] * wr[q] - wr[q] * vr[q];
+      a.d[k] = dk;
+    }
+    grid.sync();  // barrier A: x, ||x||^2 partials
+    // ---- reflector (every block, identically): vn = v_k
+    for (int64_t i = k + 1 + tid; i < n; i += bd) vn[i] = a.xbuf[i];
+    double xs = 0.0;
+    for (int bb = tid; bb < NB; bb += bd) xs += a.part_x[bb];
+    const double xn2 = block_sum_all(xs, red);
+    if (tid == 0) {
+      const double alpha = vn[k + 1];
+      double tau = 0.0, beta = alpha, scale = 0.0;
+      if (xn2 > 0.0) {
+        const double nrm = sqrt(alpha * alpha + xn2);
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      sc[0] = tau; sc[1] = beta; sc[2] = scale;
+    }
+    __syncthreads();
+    const double tau_k = sc[0], scale = sc[2];
+    for (int64_t i = k + 2 + tid; i < n; i += bd) vn[i] *= scale;
+    __syncthreads();
+    if (tid == 0) vn[k + 1] = 1.0;
+    __syncthreads();
+    if (b == 0) {
+      if (tid == 0) { a.e[k] = sc[1]; a.tau[k] = tau_k; }
+      double* h = a.hv + n * k;
+      for (int64_t i = tid; i < n; i += bd) h[i] = i >= k + 1 ? vn[i] : 0.0;
+    }
+    // ---- the previous step's v, w to global (read from the next step on, after barrier B)
+    if (l >= 1)
+      for (int64_t i = k + (int64_t)b * bd + tid; i < n; i += (int64_t)NB * bd) {
+        V[i + n * (l - 1)] = vp[i];
+        V2[i + n * (l - 1)] = vp[i];
+        W[i + n * (l - 1)] = wp[i];
+      }
+    // ---- symv on A_s: p_raw[j] = sum_{i >= k+1} A_s[i, j] v[i] for owned columns j
+    for (int64_t j = k + 1 + ((gw - (k + 1)) % GW + GW) % GW; j < n; j += GW) {
+      const double pr = column_dot<LAZY_CH>(A + n * j, k + 1, n, lane, vn);
+      if (lane == 0) a.praw[j] = pr;
+    }
+    // ---- partials of s1 = W^T v, s2 = V^T v over this block's row chunk
+    for (int q = warp; q < 2 * l; q += nw) {
+      const int lp = q < l ? q : q - l;
+      const bool isw = q < l;
+      double acc = 0.0;
+      for (int64_t i = r0 + lane; i < r1; i += 32) {
+        const double c = lp == l - 1 ? (isw ? wp[i] : vp[i]) : (isw ? W[i + n * lp] : V[i + n * lp]);
+        acc = fma(c, vn[i], acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) a.part_s[(int64_t)b * 2 * LAZY_NB + q] = acc;
+    }
+    grid.sync();  // barrier B: p_raw, the s1/s2 partials, V/W of step k-1
+    {  // s1/s2: 8 lanes per value (2l <= 64 values over 512 threads), each summing every 8th
+       // block partial with its loads issued together, then a fixed shuffle tree
+      const int q = tid >> 3, r = tid & 7;
+      double acc = 0.0;
+      if (q < 2 * l) {
+        double t[24];
+#pragma unroll
+        for (int u = 0; u < 24; ++u) {
+          const int bb = r + 8 * u;
+          t[u] = bb < NB ? a.part_s[(int64_t)bb * 2 * LAZY_NB + q] : 0.0;
+        }
+        for (int bb = r + 8 * 24; bb < NB; bb += 8) acc += a.part_s[(int64_t)bb * 2 * LAZY_NB + q];
+#pragma unroll
+        for (int u = 0; u < 24; ++u) acc += t[u];
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      if (q < 2 * l && r == 0) ss[q] = acc;
+    }
+    __syncthreads();
+    // ---- owners: p[j] = tau (p_raw[j] - sum_l' (V[j,l'] s1[l'] + W[j,l'] s2[l'])), K partial
+    double kpart = 0.0;
+    for (int64_t j = k + 1 + ((gw - (k + 1)) % GW + GW) % GW; j < n; j += GW) {
+      double corr = 0.0;
+      if (lane < l) {
+        const double vj = lane == l - 1 ? vp[j] : V[j + n * lane];
+        const double wj = lane == l - 1 ? wp[j] : W[j + n * lane];
+        corr = vj * ss[lane] + wj * ss[l + lane];
+      }
+      corr = warp_sum(corr);
+      const double pj = tau_k * (a.praw[j] - corr);
+      if (lane == 0) a.pfin[j] = pj;
+      kpart = fma(pj, vn[j], kpart);
+    }
+    const double kb = block_sum_all(lane == 0 ? kpart : 0.0, red);
+    if (tid == 0) a.part_k[b] = kb;
+    grid.sync();  // barrier C: p, K partials
+    double ks = 0.0;
+    for (int bb = tid; bb < NB; bb += bd) ks += a.part_k[bb];
+    const double K = 0.5 * tau_k * block_sum_all(ks, red);
+    for (int64_t i = tid; i < n; i += bd) {  // this step's v, w become the "previous" pair
+      const double v = i >= k + 1 ? vn[i] : 0.0;
+      vp[i] = v;
+      wp[i] = i >= k + 1 ? a.pfin[i] - K * v : 0.0;
+    }
+    __syncthreads();
+  }
+  // the last step's v, w for the panel's trailing-block GEMM (kernel end orders them)
+  const int l = a.steps;
+  if (l >= 1)
+    for (int64_t i = a.s + l - 1 + (int64_t)b * bd + tid; i < n; i += (int64_t)NB * bd) {
+      V[i + n * (l - 1)] = vp[i];
+      V2[i + n * (l - 1)] = vp[i];
+      W[i + n * (l - 1)] = wp[i];
+    }
 }
 
 // ------------------------------------------------------------------ bisection
@@ -1632,6 +1848,57 @@ static void backtransform(Ctx& c, const double* hv, const double* tau, int64_t n
   c.arena.release(mk);
 }
 
+// Lazy panels (k_sytrd_lazy + the panel's rank-2nb trailing update as two DMMA
+// GEMMs) while the trailing matrix is too large for L2; returns the first step
+// left for the column kernel. TMB_LAZY_SWITCH sets the trailing size below which
+// the column kernel takes over (default 3500: ~98 MB of fp64, about where the
+// matrix becomes L2-resident and the column kernel's single barrier per step
+// wins); TMB_LAZY=0 disables the lazy panels (A/B).
+static int64_t sytrd_lazy_panels(Ctx& c, double* A, int64_t n, int64_t k_limit, double* d, double* e, double* tau,
+                                 double* hv) {
+  static const int64_t sw = [] {
+    const char* s = std::getenv("TMB_LAZY_SWITCH");
+    return s ? std::atoll(s) : (int64_t)3500;
+  }();
+  static const bool off = [] {
+    const char* s = std::getenv("TMB_LAZY");
+    return s && std::atoi(s) == 0;
+  }();
+  if (off || n - 1 <= sw) return 0;
+  const size_t smem = sizeof(double) * (3 * (size_t)n + 33 + 8 + 4 * LAZY_NB);
+  set_smem_attr(c, (const void*)k_sytrd_lazy, std::max<size_t>(smem, 48 * 1024));
+  const int per_sm = blocks_per_sm(c, (const void*)k_sytrd_lazy, LAZY_THREADS, smem);
+  if (per_sm < 1) return 0;
+  const int blocks = (int)std::min<int64_t>((int64_t)per_sm * c.num_sms,
+                                            std::max<int64_t>(1, ceil_div(n, LAZY_THREADS / 32)));
+  const size_t mk = c.arena.mark();
+  double* VWV = alloc<double>(c, (size_t)n * 3 * LAZY_NB);
+  double* xbuf = alloc<double>(c, (size_t)n);
+  double* praw = alloc<double>(c, (size_t)n);
+  double* pfin = alloc<double>(c, (size_t)n);
+  double* part_s = alloc<double>(c, (size_t)blocks * 2 * LAZY_NB);
+  double* part_k = alloc<double>(c, (size_t)blocks);
+  double* part_x = alloc<double>(c, (size_t)blocks);
+  int64_t s = 0;
+  while (n - s - 1 > sw && s + LAZY_NB < k_limit) {
+    LazyArgs la{A, n, d, e, tau, hv, VWV, xbuf, praw, pfin, part_s, part_k, part_x, s, LAZY_NB};
+    void* args[] = {&la};
+    TMB_CUDA(cudaLaunchCooperativeKernel((const void*)k_sytrd_lazy, blocks, LAZY_THREADS, args, smem, c.stream));
+    LAUNCHED("k_sytrd_lazy");
+    const int64_t s2 = s + LAZY_NB, m = n - s2;
+    GemmDesc g;  // A[s2:, s2:] -= [V W] [W V]^T  (one rank-64 update of rows/columns >= s2)
+    g.M = m; g.N = m; g.K1 = 2 * LAZY_NB;
+    g.A = VWV + s2; g.sAm = 1; g.sAk1 = n;
+    g.B = VWV + n * LAZY_NB + s2; g.sBk1 = n; g.sBn = 1;
+    g.C = A + s2 + n * s2; g.sCm = 1; g.sCn = n;
+    g.alpha = -1.0; g.beta = 1.0;
+    gemm(c, g);
+    s = s2;
+  }
+  c.arena.release(mk);
+  return s;
+}
+
 void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs, double* vals) {
   struct TagScope {  // attribute the solver's own GEMMs (back-transform, Newton-Schulz) separately
     Ctx& c; int saved;
@@ -1703,6 +1970,7 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
     Timed timed(c, TAG_SYTRD, 4.0 / 3.0 * (double)n * n * n);  // dsytrd flop count
     static const bool rows_off = std::getenv("TMB_SYTRD_COLS") != nullptr;  // A/B: force the column kernel
     if (K0 > 0 && (rows_off || !sytrd_rows(c, A, n, K0, d, e, tau, hv, pbuf))) {
+      ta.k_begin = sytrd_lazy_panels(c, A, n, std::min<int64_t>(K0, n - 3), d, e, tau, hv);
       TMB_CUDA(cudaLaunchCooperativeKernel(kern, blocks, TRD_THREADS, args, smem, c.stream));
       LAUNCHED("k_sytrd");
     }

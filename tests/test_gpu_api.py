@@ -542,3 +542,40 @@ def test_workspace_pool_query_and_reserve():
     L.check(L.LIB.tmb_workspace_size(h, C.byref(res3), C.byref(peak)), h)
     assert res3.value == res2.value
     assert L.LIB.tmb_workspace_reserve(h, -1) != 0
+
+
+@pytest.mark.parametrize("n,k", [(2160, 270), (2500, 97)])
+def test_eig_lazy_panels_forced_vs_lapack(n, k):
+    """The lazy (blocked) tridiagonalisation panels, forced down to trailing size
+    1000 (TMB_LAZY_SWITCH; by default they only run while the trailing matrix
+    exceeds 3500, i.e. at the C5 / C4 sizes tested above): several 32-step panels,
+    the rank-64 trailing GEMM updates, then the column kernel from the hand-off
+    step. Same accuracy contract as LAPACK."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    code = f"""
+import sys; sys.path[:0] = [{str(root)!r}, {str(root / 'tests')!r}]
+import numpy as np, oracle, paper_2104_04726_b200 as tb
+from conftest import principal_angle
+n, k = {n}, {k}
+rng = np.random.default_rng(n + k)
+q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+lam = 1e3 * np.exp(-np.linspace(0, 18, n))
+g = (q * lam) @ q.T
+g = 0.5 * (g + g.T)
+v, w = tb.leading_eigvecs(g, k)
+vr, wr = oracle.leading_eigvecs(g, k)
+assert np.abs(v.T @ v - np.eye(k)).max() < 1e-12
+assert np.abs(w - wr).max() / wr[0] < 1e-13
+assert np.abs(g @ v - v * w).max() / wr[0] < 1e-12
+assert principal_angle(v, vr) < 1e-8
+assert np.abs(v - vr).max() < 1e-8
+print("ok")
+"""
+    env = dict(os.environ, TMB_LAZY_SWITCH="1000")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-3000:]

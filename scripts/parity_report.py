@@ -38,7 +38,8 @@ def report(label, res, z, tag=""):
         lv = res.levels.ravel(order="F").astype(np.int64)
         if f"{tag}levels" in z:
             r = z[f"{tag}levels"].astype(np.int64)
-            mine = lv
+            mine = lv if r.ndim == 1 else res.levels.astype(np.int64)
+            r, mine = r.ravel(), mine.ravel()
         else:
             r = z[f"{tag}levels_sample"].astype(np.int64)
             mine = lv[z[f"{tag}levels_idx"]]

@@ -149,6 +149,11 @@ int tmb_mode_gram(tmb_ctx* ctx, const void* x_dev, int dtype, int order, const i
  * max-|entry| is positive. vecs column-major n x k. */
 int tmb_leading_eigvecs(tmb_ctx* ctx, const double* g_dev, int64_t n, int64_t k,
                         double* vecs_dev, double* vals_dev);
+/* The tridiagonal form T = Q^T g Q behind leading_eigvecs for large n (the
+ * two-stage reduction: dense -> band of half-bandwidth 32 -> tridiagonal; the
+ * reference reaches the same T inside eigh, tensor.py:195). d: n diagonal,
+ * e: n-1 subdiagonal entries (device). n >= 3. */
+int tmb_tridiagonalize(tmb_ctx* ctx, const double* g_dev, int64_t n, double* d_dev, double* e_dev);
 /* fro_norm^2 (tensor.py:212-214), deterministic fp64 reduction; host result. */
 int tmb_sumsq(tmb_ctx* ctx, const void* x_dev, int dtype, int64_t n, double* out_host);
 

@@ -75,6 +75,7 @@ SIGNATURES = {
     "tmb_mirror_upper": ([_vp, _vp, _i64], _int),
     "tmb_mode_gram": ([_vp, _vp, _int, _int, _pi64, _int, _vp], _int),
     "tmb_leading_eigvecs": ([_vp, _vp, _i64, _i64, _vp, _vp], _int),
+    "tmb_tridiagonalize": ([_vp, _vp, _i64, _vp, _vp], _int),
     "tmb_sumsq": ([_vp, _vp, _int, _i64, C.POINTER(_dbl)], _int),
     "tmb_resid_sumsq": ([_vp, _vp, _int, _vp, _i64, C.POINTER(_dbl)], _int),
     "tmb_axpy": ([_vp, _i64, _dbl, _vp, _vp], _int),

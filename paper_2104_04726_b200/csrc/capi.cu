@@ -270,6 +270,25 @@ int tmb_leading_eigvecs(tmb_ctx* ctx, const double* g, int64_t n, int64_t k, dou
   });
 }
 
+int tmb_tridiagonalize(tmb_ctx* ctx, const double* g, int64_t n, double* d, double* e) {
+  return guard(ctx, [&](tmb::Ctx& c) {
+    if (n < 3) throw Error(TMB_EINVAL, "tridiagonalize: n must be >= 3");
+    const size_t mk = c.arena.mark();
+    double* A = tmb::alloc<double>(c, (size_t)n * n);
+    double* hv = tmb::alloc<double>(c, (size_t)n * n);
+    double* tau = tmb::alloc<double>(c, (size_t)n);
+    double* band = tmb::alloc<double>(c, (size_t)n * (2 * tmb::SBR_B + 1));
+    TMB_CUDA(cudaMemsetAsync(hv, 0, sizeof(double) * n * n, c.stream));
+    TMB_CUDA(cudaMemsetAsync(tau, 0, sizeof(double) * n, c.stream));
+    tmb::copy_d(c, A, g, n * n);
+    tmb::sy2sb(c, A, n, hv, tau);
+    tmb::band_rows(c, A, n, band);
+    tmb::sb2st(c, band, n, d, e);
+    TMB_CUDA(cudaStreamSynchronize(c.stream));
+    c.arena.release(mk);
+  });
+}
+
 int tmb_sumsq(tmb_ctx* ctx, const void* x, int dtype, int64_t n, double* out) {
   return guard(ctx, [&](tmb::Ctx& c) { *out = tmb::sumsq(c, x, to_dtype(dtype), n); });
 }

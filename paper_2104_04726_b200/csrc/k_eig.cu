@@ -1899,6 +1899,71 @@ static int64_t sytrd_lazy_panels(Ctx& c, double* A, int64_t n, int64_t k_limit, 
   return s;
 }
 
+// Top-k eigenvalues of tridiag(d, e), descending, by multisection.
+static void bisect_top(Ctx& c, const double* d, const double* e, int64_t n, int64_t k, double* vals) {
+  // 2 warps (eigenvalues) per block: the counts are FP64-throughput bound, so
+  // spread the k warps over all SMs (k/8 blocks of 8 warps left 60 % idle)
+  static const int bis_w = [] {
+    const char* s = std::getenv("TMB_BISECT_WARPS");  // A/B: warps per eigenvalue (1, 2, 4)
+    return s ? std::atoi(s) : 2;  // measured: 1.15 / 1.25 / 1.37 ms tridiag at n=1920 for 2 / 1 / 4
+  }();
+  if (bis_w == 4) k_bisect_mw<4><<<(unsigned)k, 128, 0, c.stream>>>(d, e, n, k, vals);
+  else if (bis_w == 2) k_bisect_mw<2><<<(unsigned)k, 64, 0, c.stream>>>(d, e, n, k, vals);
+  else k_bisect<<<(unsigned)ceil_div(k, 2), 64, 0, c.stream>>>(d, e, n, k, vals);
+  LAUNCHED("k_bisect");
+}
+
+// Two-stage path (k_twostage.cu): dense -> band (cluster panel QR + DMMA
+// trailing updates) -> tridiagonal (cluster bulge chasing) -> eigenvalues by
+// multisection -> eigenvectors of the band by inverse iteration -> stage-1
+// reflectors back-applied in compact-WY panels -> Newton-Schulz.
+// TMB_EIG_2STAGE=1 selects it (tests, A/B runs). Returns false,
+// with nothing written but scratch, when the vectors of a tight eigenvalue
+// cluster came out (nearly) parallel: the caller then runs the one-stage path,
+// whose cluster repair works on the tridiagonal matrix.
+static bool two_stage_for(int64_t n) {
+  static const int mode = [] {
+    const char* s = std::getenv("TMB_EIG_2STAGE");
+    return s ? std::atoi(s) : -1;
+  }();
+  if (n < 4 * SBR_B || mode == 0) return false;
+  return mode == 1;  // opt-in until it beats the one-stage path
+}
+
+static bool eig_two_stage(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs, double* vals) {
+  const size_t mk = c.arena.mark();
+  const int64_t hv_cols = ceil_div(n, wy_nb()) * wy_nb();
+  double* A = alloc<double>(c, (size_t)n * n);
+  double* hv = alloc<double>(c, (size_t)n * hv_cols);
+  double* tau = alloc<double>(c, hv_cols);
+  double* band = alloc<double>(c, (size_t)n * (2 * SBR_B + 1));
+  double* d = alloc<double>(c, n);
+  double* e = alloc<double>(c, n);
+  TMB_CUDA(cudaMemsetAsync(hv, 0, sizeof(double) * n * hv_cols, c.stream));
+  TMB_CUDA(cudaMemsetAsync(tau, 0, sizeof(double) * hv_cols, c.stream));
+  copy_d(c, A, g, n * n);
+  {
+    Timed timed(c, TAG_SYTRD, 4.0 / 3.0 * (double)n * n * n);
+    sy2sb(c, A, n, hv, tau);
+    band_rows(c, A, n, band);
+    sb2st(c, band, n, d, e);
+  }
+  {
+    Timed timed_tri(c, TAG_TRIDIAG, 0.0);
+    bisect_top(c, d, e, n, k, vals);
+    band_invit(c, band, n, k, vals, vecs);
+  }
+  backtransform(c, hv, tau, n, hv_cols, k, vecs);
+  const double e0 = orthonormalize(c, vecs, n, k, kRepairOrtho);
+  static const bool stats = std::getenv("TMB_EIG_STATS") != nullptr;
+  if (stats) std::fprintf(stderr, "leading_eigvecs(2-stage) n=%lld k=%lld max|X^T X - I| = %.3e\n", (long long)n,
+                          (long long)k, e0);
+  c.arena.release(mk);
+  if (!(e0 < kRepairOrtho)) return false;
+  sign_fix(c, vecs, n, k);
+  return true;
+}
+
 void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs, double* vals) {
   struct TagScope {  // attribute the solver's own GEMMs (back-transform, Newton-Schulz) separately
     Ctx& c; int saved;
@@ -1913,6 +1978,7 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
     LAUNCHED("k_jacobi");
     return;
   }
+  if (two_stage_for(n) && eig_two_stage(c, g, n, k, vecs, vals)) return;
   const size_t mk = c.arena.mark();
   double* A = alloc<double>(c, (size_t)n * n);
   // Householder vectors: columns 0..n-3 written by k_sytrd, the rest (up to a
@@ -2000,14 +2066,7 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
     Timed timed_tri(c, TAG_TRIDIAG, 0.0);
     // 2 warps (eigenvalues) per block: the counts are FP64-throughput bound, so
     // spread the k warps over all SMs (k/8 blocks of 8 warps left 60 % idle)
-    static const int bis_w = [] {
-      const char* s = std::getenv("TMB_BISECT_WARPS");  // A/B: warps per eigenvalue (1, 2, 4)
-      return s ? std::atoi(s) : 2;  // measured: 1.15 / 1.25 / 1.37 ms tridiag at n=1920 for 2 / 1 / 4
-    }();
-    if (bis_w == 4) k_bisect_mw<4><<<(unsigned)k, 128, 0, c.stream>>>(d, e, n, k, vals);
-    else if (bis_w == 2) k_bisect_mw<2><<<(unsigned)k, 64, 0, c.stream>>>(d, e, n, k, vals);
-    else k_bisect<<<(unsigned)ceil_div(k, 2), 64, 0, c.stream>>>(d, e, n, k, vals);
-    LAUNCHED("k_bisect");
+    bisect_top(c, d, e, n, k, vals);
     static const bool tw_global = std::getenv("TMB_TWISTED_GLOBAL") != nullptr;  // A/B: L2 scratch variant
     const size_t tw_smem = sizeof(double) * 2 * (size_t)n;  // per eigenvalue
     run_twisted = [&, tw_smem]() {

@@ -164,6 +164,19 @@ void sytrd_tail(Ctx& c, double* A, int64_t n, int64_t K0, double* d, double* e, 
 int64_t sytrd_tail1_max();
 void sytrd_tail1(Ctx& c, double* A, int64_t n, int64_t K0, double* d, double* e, double* tau, double* hv);
 
+// ---------------------------------------------------------------- two-stage tridiagonalisation (k_twostage.cu)
+constexpr int SBR_B = 32;  // half-bandwidth of the intermediate band matrix
+// stage 1: symmetric A (n x n, column-major) -> band of half-bandwidth SBR_B in place
+// (entries outside the band are left undefined); reflector of column c in hv column c
+// (zero above its first row; hv and tau must be zeroed by the caller)
+void sy2sb(Ctx& c, double* A, int64_t n, double* hv, double* tau);
+// the band of A as full rows: band[r * (2 SBR_B + 1) + (col - r + SBR_B)]
+void band_rows(Ctx& c, const double* A, int64_t n, double* band);
+// stage 2: band -> tridiagonal (d: n diagonal, e: n-1 subdiagonal)
+void sb2st(Ctx& c, const double* band, int64_t n, double* d, double* e);
+// unit eigenvectors of the band matrix for the k eigenvalues vals (n x k, column-major)
+void band_invit(Ctx& c, const double* band, int64_t n, int64_t k, const double* vals, double* z);
+
 // ---------------------------------------------------------------- colour (k_color.cu)
 void color_u8(Ctx& c, const uint8_t* rgb, int64_t n_img, int64_t h, int64_t w, int space, float* out,
               bool channel_major = false);

@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
+mkdir -p gpurun_out
+timeout 120 python scripts/prof_twostage.py 1000 > gpurun_out/n3_plain.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sb2st|k_band_invit" -c 2 -o gpurun_out/s3_sb2st_full python scripts/prof_twostage.py 1000 > gpurun_out/n3_ncu.log 2>&1
+echo rc=$?
+tail -2 gpurun_out/n3_ncu.log

@@ -1917,7 +1917,8 @@ static void bisect_top(Ctx& c, const double* d, const double* e, int64_t n, int6
 // trailing updates) -> tridiagonal (cluster bulge chasing) -> eigenvalues by
 // multisection -> eigenvectors of the band by inverse iteration -> stage-1
 // reflectors back-applied in compact-WY panels -> Newton-Schulz.
-// TMB_EIG_2STAGE=1 selects it (tests, A/B runs). Returns false,
+// Default for n > 6000 (C5's n = 7680 Gram); TMB_EIG_2STAGE=1 forces it
+// (tests, A/B runs), =0 disables it. Returns false,
 // with nothing written but scratch, when the vectors of a tight eigenvalue
 // cluster came out (nearly) parallel: the caller then runs the one-stage path,
 // whose cluster repair works on the tridiagonal matrix.
@@ -1927,7 +1928,9 @@ static bool two_stage_for(int64_t n) {
     return s ? std::atoi(s) : -1;
   }();
   if (n < 4 * SBR_B || mode == 0) return false;
-  return mode == 1;  // opt-in until it beats the one-stage path
+  // measured crossover (scripts/gpu_s3_ab.sh): n = 7680 278 vs 413 ms (k = 960),
+  // n = 4320 115 vs 95 ms, n = 3840 101 vs 71 ms, n = 2160 51 vs 19 ms
+  return mode == 1 || n > 6000;
 }
 
 static bool eig_two_stage(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs, double* vals) {

@@ -249,11 +249,11 @@ __global__ void __launch_bounds__(SB) k_larft32(const double* __restrict__ S, co
   for (int i = 0; i < SB; ++i) T[r + SB * i] = tr[i];
 }
 
-// W = X - V (T^T M) / 2 for the m panel rows; writes [V | W | V] (m x 96, ld m)
+// W = X - V (T^T M) / 2 for the m panel rows; writes [V | W | V] (m x 96, ld ldo)
 // so the trailing update A22 -= V W^T + W V^T is one GEMM with plain strides.
 __global__ void __launch_bounds__(256) k_sbr_w(const double* __restrict__ X, const double* __restrict__ V, int64_t ldv,
                                                const double* __restrict__ M, const double* __restrict__ T, int64_t m,
-                                               double* __restrict__ VWV) {
+                                               double* __restrict__ VWV, int64_t ldo) {
   __shared__ double sZ[SB * SB], sM[SB * SB], sT[SB * SB];
   const int tid = threadIdx.x;
   for (int e = tid; e < SB * SB; e += 256) { sM[e] = M[e]; sT[e] = T[e]; }
@@ -272,9 +272,9 @@ __global__ void __launch_bounds__(256) k_sbr_w(const double* __restrict__ X, con
 #pragma unroll 8
     for (int k = 0; k < SB; ++k) s = fma(V[r + ldv * k], sZ[k + SB * cc], s);
     const double v = V[r + ldv * cc];
-    VWV[r + m * cc] = v;
-    VWV[r + m * (SB + cc)] = fma(-0.5, s, X[r + m * cc]);
-    VWV[r + m * (2 * SB + cc)] = v;
+    VWV[r + ldo * cc] = v;
+    VWV[r + ldo * (SB + cc)] = fma(-0.5, s, X[r + m * cc]);
+    VWV[r + ldo * (2 * SB + cc)] = v;
   }
 }
 
@@ -293,7 +293,8 @@ __global__ void k_band_rows(const double* __restrict__ A, int64_t n, double* __r
 // ------------------------------------------------------------------ stage 2: bulge chasing
 constexpr int S2_W = 8;            // worker warps per CTA (one task each)
 constexpr int S2_NS = 32;          // progress / mailbox slots (sweep mod S2_NS)
-constexpr int S2_LDL = 2 * SB + 1; // lower band row: offsets 0 .. 2b-1 (+1 pad)
+constexpr int S2_LDL = 2 * SB;     // lower band row: offsets 0 .. 2b-1 (stride 64: the diagonal walks at
+                                   // stride 65 are bank-conflict free, 65 made them 2-way)
 
 struct S2Args {
   const double* band;
@@ -435,9 +436,10 @@ __device__ __forceinline__ void s2_task(const Acc& acc, int j, int m, int lane, 
 // base + i * S2_LDL, so every access is a shared load/store at a lane base
 // plus an immediate (row stride 65 doubles: column walks are conflict-free).
 __device__ __forceinline__ void s2_task_fast(double* base, int j, int lane, double vp, double taup, double* vs,
-                                             double* ws, double* zs, double& v, double& tau) {
+                                             double* ws, double* zs, double& v, double& tau, long long* ph) {
   double* rp = base + lane * S2_LDL;
   double beta;
+  long long c0 = clock64(), c1 = c0, c2 = c0, c3 = c0;
   if (j == 0) {
     const double x = rp[1 + lane];  // column s, rows q0 + lane
     house_warp(x, lane, v, tau, beta);
@@ -461,7 +463,9 @@ __device__ __forceinline__ void s2_task_fast(double* base, int j, int lane, doub
       brow[jj] = fma(-ty, vs[jj], brow[jj]);
       bp[-jj] = brow[jj];
     }
+    c1 = clock64();
     house_warp(brow[0], lane, v, tau, beta);
+    c2 = clock64();
     ws[lane] = v;
     __syncwarp();
     // z_lane = sum_i v_i B[i][lane] = sum_i v_i L[q0+i][SB+i-lane]: column walk
@@ -479,6 +483,7 @@ __device__ __forceinline__ void s2_task_fast(double* base, int j, int lane, doub
     for (int jj = 1; jj < SB; ++jj) bp[-jj] = fma(-v, zs[jj], brow[jj]);
   }
   __syncwarp();
+  c3 = clock64();
   // D: the lane's full symmetric row; D[lane][c] = L[q0+lane][lane-c] (c <= lane)
   // or L[q0+c][c-lane] = rp[(c - lane) * (S2_LDL + 1)] (c > lane)
   double drow[SB];
@@ -505,6 +510,11 @@ __device__ __forceinline__ void s2_task_fast(double* base, int j, int lane, doub
 #pragma unroll
   for (int cc = 0; cc < SB; ++cc)
     if (cc <= lane) up[-cc] = fma(-v, ws[cc], fma(-w, vs[cc], drow[cc]));
+  __syncwarp();
+  if (ph && j > 0) {
+    const long long c4 = clock64();
+    ph[0] += c1 - c0; ph[1] += c2 - c1; ph[2] += c3 - c2; ph[3] += c4 - c3; ph[4] += 1;
+  }
 }
 
 template <int CS>
@@ -557,6 +567,7 @@ __global__ void __launch_bounds__(S2_W * 32, 1) k_sb2st(const S2Args a) {
   double* ws = vs + 32;
   double* zs = vs + 64;
   long long pw = 0, pt = 0, pn = 0;
+  long long ph[5] = {0, 0, 0, 0, 0};
   for (int s = warp; s <= n - 3; s += S2_W) {
     if (s + 1 >= hi) break;
     const int jst = lo > s + 1 ? (lo - s - 1 + SB - 1) / SB : 0;
@@ -584,7 +595,7 @@ __global__ void __launch_bounds__(S2_W * 32, 1) k_sb2st(const S2Args a) {
       const int m = min(SB, n - q0);
       double v, tau;
       if (m == SB && q0 + m <= lo + min(RS, hi - lo)) {  // every row of the block in this CTA's shared memory
-        s2_task_fast(rows + (size_t)(q0 - lo) * S2_LDL, j, lane, vp, taup, vs, ws, zs, v, tau);
+        s2_task_fast(rows + (size_t)(q0 - lo) * S2_LDL, j, lane, vp, taup, vs, ws, zs, v, tau, a.prof ? ph : nullptr);
       } else {
         S2Gen acc{rows, rows_nx, a.spill, q0, lo, hi, R, RS, cr};
         s2_task(acc, j, m, lane, vp, taup, vs, ws, zs, v, tau);
@@ -611,8 +622,9 @@ __global__ void __launch_bounds__(S2_W * 32, 1) k_sb2st(const S2Args a) {
     }
   }
   if (a.prof && lane == 0) {
-    long long* q = a.prof + 3 * (blockIdx.x * S2_W + warp);
+    long long* q = a.prof + 8 * (blockIdx.x * S2_W + warp);
     q[0] = pw; q[1] = pt; q[2] = pn;
+    for (int t = 0; t < 5; ++t) q[3 + t] = ph[t];
   }
   if constexpr (CS > 1) cl.sync(); else __syncthreads();
   for (int r = lo + tid; r < hi; r += S2_W * 32) {
@@ -902,7 +914,20 @@ __global__ void __launch_bounds__(IV_W * 32) k_band_invit(const double* __restri
 
 }  // namespace
 
+// Panels are processed in groups of G with the trailing update deferred to the
+// end of the group (one DMMA GEMM with K = 64 G instead of G GEMMs with K = 64,
+// which were bound by the C-tile traffic at K = 64). Inside a group, panel q
+// first brings its own columns (and diagonal block) up to date, and its X uses
+// the stale trailing matrix plus the pending terms (dlatrd's device, restated):
+//   X = (A - sum_{q'<q} V_q' W_q'^T + W_q' V_q'^T) VT = A VT - [V W]_{q'} ([W V]_{q'}^T VT).
+// The pending [V_q W_q V_q] triples live side by side in VWg (rows from the
+// group's first reflector row rg, zero above each panel's own rows).
 void sy2sb(Ctx& c, double* A, int64_t n, double* hv, double* tau) {
+  static const int genv = [] {
+    const char* e = std::getenv("TMB_SBR_GROUP");  // A/B: panels per deferred trailing update
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
+  const int G = genv ? genv : (n > 3000 ? 4 : 2);
   const size_t mk = c.arena.mark();
   const int64_t mmax = n - SB;
   double* S = alloc<double>(c, SB * SB);
@@ -910,62 +935,96 @@ void sy2sb(Ctx& c, double* A, int64_t n, double* hv, double* tau) {
   double* M = alloc<double>(c, SB * SB);
   double* VT = alloc<double>(c, (size_t)mmax * SB);
   double* X = alloc<double>(c, (size_t)mmax * SB);
-  double* VWV = alloc<double>(c, (size_t)mmax * 3 * SB);
-  for (int64_t p0 = 0; p0 + SB < n - 1; p0 += SB) {
-    const int64_t r0 = p0 + SB, m = n - r0;
-    PanelArgs pa{A, n, p0, hv, tau};
-    if (m <= PQ_NT) panel_qr_cs<1>(c, pa);
-    else if (m <= 2 * PQ_NT) panel_qr_cs<2>(c, pa);
-    else if (m <= 4 * PQ_NT) panel_qr_cs<4>(c, pa);
-    else if (m <= 8 * PQ_NT) panel_qr_cs<8>(c, pa);
-    else if (m <= 16 * PQ_NT) panel_qr_cs<16>(c, pa);
-    else throw Error(TMB_EINVAL, "sy2sb: matrix too large for the cluster panel factorisation");
-    const double* V = hv + r0 + n * p0;  // m x 32, ld n
-    {  // S = V^T V
-      GemmDesc g;
-      g.M = SB; g.N = SB; g.K1 = m;
-      g.A = V; g.sAm = n; g.sAk1 = 1;
-      g.B = V; g.sBk1 = 1; g.sBn = n;
-      g.C = S; g.sCm = 1; g.sCn = SB;
-      gemm(c, g);
+  double* Yc = alloc<double>(c, (size_t)G * 2 * SB * SB);
+  double* VWg = alloc<double>(c, (size_t)mmax * 3 * SB * G);
+  for (int64_t g0 = 0; g0 + SB < n - 1; g0 += (int64_t)G * SB) {
+    const int64_t rg = g0 + SB, ldw = n - rg;
+    TMB_CUDA(cudaMemsetAsync(VWg, 0, sizeof(double) * ldw * 3 * SB * G, c.stream));
+    int q = 0;
+    for (; q < G; ++q) {
+      const int64_t p0 = g0 + q * SB, r0 = p0 + SB;
+      if (!(p0 + SB < n - 1)) break;
+      const int64_t m = n - r0;
+      if (q > 0) {  // A[p0:, p0:p0+32] -= sum_{q'<q} [V W] [W V]^T (rows p0.., columns of this panel)
+        GemmDesc g;
+        g.M = n - p0; g.N = SB; g.K1 = 2 * SB; g.K2 = q;
+        g.A = VWg + (p0 - rg); g.sAm = 1; g.sAk1 = ldw; g.sAk2 = 3 * SB * ldw;
+        g.B = VWg + (p0 - rg) + SB * ldw; g.sBn = 1; g.sBk1 = ldw; g.sBk2 = 3 * SB * ldw;
+        g.C = A + p0 + n * p0; g.sCm = 1; g.sCn = n;
+        g.alpha = -1.0; g.beta = 1.0;
+        gemm(c, g);
+      }
+      PanelArgs pa{A, n, p0, hv, tau};
+      if (m <= PQ_NT) panel_qr_cs<1>(c, pa);
+      else if (m <= 2 * PQ_NT) panel_qr_cs<2>(c, pa);
+      else if (m <= 4 * PQ_NT) panel_qr_cs<4>(c, pa);
+      else if (m <= 8 * PQ_NT) panel_qr_cs<8>(c, pa);
+      else if (m <= 16 * PQ_NT) panel_qr_cs<16>(c, pa);
+      else throw Error(TMB_EINVAL, "sy2sb: matrix too large for the cluster panel factorisation");
+      const double* V = hv + r0 + n * p0;  // m x 32, ld n
+      {  // S = V^T V
+        GemmDesc g;
+        g.M = SB; g.N = SB; g.K1 = m;
+        g.A = V; g.sAm = n; g.sAk1 = 1;
+        g.B = V; g.sBk1 = 1; g.sBn = n;
+        g.C = S; g.sCm = 1; g.sCn = SB;
+        gemm(c, g);
+      }
+      k_larft32<<<1, SB, 0, c.stream>>>(S, tau + p0, T);
+      LAUNCHED("k_larft32");
+      {  // VT = V T
+        GemmDesc g;
+        g.M = m; g.N = SB; g.K1 = SB;
+        g.A = V; g.sAm = 1; g.sAk1 = n;
+        g.B = T; g.sBk1 = 1; g.sBn = SB;
+        g.C = VT; g.sCm = 1; g.sCn = m;
+        gemm(c, g);
+      }
+      {  // X = A22 VT (A22 stale by the group's pending updates)
+        GemmDesc g;
+        g.M = m; g.N = SB; g.K1 = m;
+        g.A = A + r0 + n * r0; g.sAm = 1; g.sAk1 = n;
+        g.B = VT; g.sBk1 = 1; g.sBn = m;
+        g.C = X; g.sCm = 1; g.sCn = m;
+        gemm(c, g);
+      }
+      if (q > 0) {
+        GemmDesc y;  // Yc[q'] = [W V]_{q', rows r0..}^T VT  (64 x 32 per pending panel)
+        y.M = 2 * SB; y.N = SB; y.K1 = m; y.batch = q;
+        y.A = VWg + (r0 - rg) + SB * ldw; y.sAm = ldw; y.sAk1 = 1; y.sAb = 3 * SB * ldw;
+        y.B = VT; y.sBk1 = 1; y.sBn = m; y.sBb = 0;
+        y.C = Yc; y.sCm = 1; y.sCn = 2 * SB; y.sCb = 2 * SB * SB;
+        gemm(c, y);
+        GemmDesc x2;  // X -= [V W]_{q', rows r0..} Yc[q']
+        x2.M = m; x2.N = SB; x2.K1 = 2 * SB; x2.K2 = q;
+        x2.A = VWg + (r0 - rg); x2.sAm = 1; x2.sAk1 = ldw; x2.sAk2 = 3 * SB * ldw;
+        x2.B = Yc; x2.sBk1 = 1; x2.sBk2 = 2 * SB * SB; x2.sBn = 2 * SB;
+        x2.C = X; x2.sCm = 1; x2.sCn = m;
+        x2.alpha = -1.0; x2.beta = 1.0;
+        gemm(c, x2);
+      }
+      {  // M = V^T X
+        GemmDesc g;
+        g.M = SB; g.N = SB; g.K1 = m;
+        g.A = V; g.sAm = n; g.sAk1 = 1;
+        g.B = X; g.sBk1 = 1; g.sBn = m;
+        g.C = M; g.sCm = 1; g.sCn = SB;
+        gemm(c, g);
+      }
+      k_sbr_w<<<(unsigned)std::min<int64_t>(ceil_div(m, 8), 4 * c.num_sms), 256, 0, c.stream>>>(
+          X, V, n, M, T, m, VWg + (r0 - rg) + (int64_t)3 * SB * q * ldw, ldw);
+      LAUNCHED("k_sbr_w");
     }
-    k_larft32<<<1, SB, 0, c.stream>>>(S, tau + p0, T);
-    LAUNCHED("k_larft32");
-    {  // VT = V T
-      GemmDesc g;
-      g.M = m; g.N = SB; g.K1 = SB;
-      g.A = V; g.sAm = 1; g.sAk1 = n;
-      g.B = T; g.sBk1 = 1; g.sBn = SB;
-      g.C = VT; g.sCm = 1; g.sCn = m;
-      gemm(c, g);
-    }
-    double* A22 = A + r0 + n * r0;
-    {  // X = A22 VT
-      GemmDesc g;
-      g.M = m; g.N = SB; g.K1 = m;
-      g.A = A22; g.sAm = 1; g.sAk1 = n;
-      g.B = VT; g.sBk1 = 1; g.sBn = m;
-      g.C = X; g.sCm = 1; g.sCn = m;
-      gemm(c, g);
-    }
-    {  // M = V^T X
-      GemmDesc g;
-      g.M = SB; g.N = SB; g.K1 = m;
-      g.A = V; g.sAm = n; g.sAk1 = 1;
-      g.B = X; g.sBk1 = 1; g.sBn = m;
-      g.C = M; g.sCm = 1; g.sCn = SB;
-      gemm(c, g);
-    }
-    k_sbr_w<<<(unsigned)std::min<int64_t>(ceil_div(m, 8), 4 * c.num_sms), 256, 0, c.stream>>>(X, V, n, M, T, m, VWV);
-    LAUNCHED("k_sbr_w");
-    {  // A22 -= [V W] [W V]^T
-      GemmDesc g;
-      g.M = m; g.N = m; g.K1 = 2 * SB;
-      g.A = VWV; g.sAm = 1; g.sAk1 = m;
-      g.B = VWV + m * SB; g.sBk1 = m; g.sBn = 1;
-      g.C = A22; g.sCm = 1; g.sCn = n;
-      g.alpha = -1.0; g.beta = 1.0;
-      gemm(c, g);
+    // the group's deferred two-sided update of everything right of / below its panels
+    const int64_t pn = g0 + (int64_t)q * SB;
+    if (q > 0 && pn < n) {
+      GemmDesc u;
+      u.M = n - pn; u.N = n - pn; u.K1 = 2 * SB; u.K2 = q;
+      u.A = VWg + (pn - rg); u.sAm = 1; u.sAk1 = ldw; u.sAk2 = 3 * SB * ldw;
+      u.B = VWg + (pn - rg) + SB * ldw; u.sBn = 1; u.sBk1 = ldw; u.sBk2 = 3 * SB * ldw;
+      u.C = A + pn + n * pn; u.sCm = 1; u.sCn = n;
+      u.alpha = -1.0; u.beta = 1.0;
+      gemm(c, u);
     }
   }
   c.arena.release(mk);
@@ -993,22 +1052,28 @@ void sb2st_cs(Ctx& c, const double* band, int n, double* d, double* e) {
   static const bool prof_on = std::getenv("TMB_S2_PROF") != nullptr;
   long long* prof = nullptr;
   if (prof_on) {
-    prof = alloc<long long>(c, (size_t)CS * S2_W * 3);
-    TMB_CUDA(cudaMemsetAsync(prof, 0, sizeof(long long) * CS * S2_W * 3, c.stream));
+    prof = alloc<long long>(c, (size_t)CS * S2_W * 8);
+    TMB_CUDA(cudaMemsetAsync(prof, 0, sizeof(long long) * CS * S2_W * 8, c.stream));
   }
   S2Args a{band, n, R, RS, spill, d, e, prof};
   void* args[] = {&a};
   launch_cluster(c, k_sb2st<CS>, CS, dim3(CS), S2_W * 32, smem, args);
   LAUNCHED("k_sb2st");
   if (prof) {
-    std::vector<long long> h((size_t)CS * S2_W * 3);
+    std::vector<long long> h((size_t)CS * S2_W * 8);
     TMB_CUDA(cudaMemcpyAsync(h.data(), prof, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, c.stream));
     TMB_CUDA(cudaStreamSynchronize(c.stream));
     for (int b = 0; b < CS; ++b) {
-      long long w = 0, t = 0, k = 0;
-      for (int q = 0; q < S2_W; ++q) { w += h[(b * S2_W + q) * 3]; t += h[(b * S2_W + q) * 3 + 1]; k += h[(b * S2_W + q) * 3 + 2]; }
-      std::fprintf(stderr, "sb2st n=%d CTA %d: tasks %lld, cycles/task %.0f, wait cycles/task %.0f\n", n, b, k,
-                   k ? (double)t / k : 0.0, k ? (double)w / k : 0.0);
+      long long w = 0, t = 0, k = 0, f[5] = {0, 0, 0, 0, 0};
+      for (int q = 0; q < S2_W; ++q) {
+        const long long* r = &h[(b * S2_W + q) * 8];
+        w += r[0]; t += r[1]; k += r[2];
+        for (int u = 0; u < 5; ++u) f[u] += r[3 + u];
+      }
+      const double fk = f[4] ? (double)f[4] : 1.0;
+      std::fprintf(stderr, "sb2st n=%d CTA %d: tasks %lld, cycles/task %.0f, wait cycles/task %.0f | fast tasks %lld: "
+                   "right %.0f house %.0f left %.0f diag %.0f\n", n, b, k, k ? (double)t / k : 0.0,
+                   k ? (double)w / k : 0.0, f[4], f[0] / fk, f[1] / fk, f[2] / fk, f[3] / fk);
     }
   }
   c.arena.release(mk);

@@ -1917,7 +1917,7 @@ static void bisect_top(Ctx& c, const double* d, const double* e, int64_t n, int6
 // trailing updates) -> tridiagonal (cluster bulge chasing) -> eigenvalues by
 // multisection -> eigenvectors of the band by inverse iteration -> stage-1
 // reflectors back-applied in compact-WY panels -> Newton-Schulz.
-// Default for n > 6000 (C5's n = 7680 Gram); TMB_EIG_2STAGE=1 forces it
+// Default for n > 4000 (C5's n = 4320 and 7680 Grams); TMB_EIG_2STAGE=1 forces it
 // (tests, A/B runs), =0 disables it. Returns false,
 // with nothing written but scratch, when the vectors of a tight eigenvalue
 // cluster came out (nearly) parallel: the caller then runs the one-stage path,
@@ -1928,9 +1928,10 @@ static bool two_stage_for(int64_t n) {
     return s ? std::atoi(s) : -1;
   }();
   if (n < 4 * SBR_B || mode == 0) return false;
-  // measured crossover (scripts/gpu_s3_ab.sh): n = 7680 278 vs 413 ms (k = 960),
-  // n = 4320 115 vs 95 ms, n = 3840 101 vs 71 ms, n = 2160 51 vs 19 ms
-  return mode == 1 || n > 6000;
+  // measured crossover (scripts/gpu_s3_ab.sh, two-stage vs one-stage): n = 7680
+  // 239 vs 410 ms (k = 960), n = 4320 92 vs 95 ms (k = 540), n = 3840 82 vs 71 ms
+  // (k = 960), n = 2160 40 vs 19 ms
+  return mode == 1 || n > 4000;
 }
 
 static bool eig_two_stage(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs, double* vals) {

@@ -94,31 +94,6 @@ __device__ __forceinline__ double rs_row(const double (&row)[SB], double x, int 
   return v[0];
 }
 
-// reduce-scatter of val_t = v * b[t] (first stage formed on the fly)
-__device__ __forceinline__ double rs_scaled(const double (&b)[SB], double v, int lane) {
-  double u[16];
-  {
-    const bool up = lane & 16;
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      const double a0 = v * b[t], a1 = v * b[t + 16];
-      const double send = up ? a0 : a1, keep = up ? a1 : a0;
-      u[t] = keep + __shfl_xor_sync(FULL, send, 16);
-    }
-  }
-#pragma unroll
-  for (int o = 8; o >= 1; o >>= 1) {
-    const bool up = lane & o;
-#pragma unroll
-    for (int t = 0; t < o; ++t) {
-      const double send = up ? u[t] : u[t + o];
-      const double keep = up ? u[t + o] : u[t];
-      u[t] = keep + __shfl_xor_sync(FULL, send, o);
-    }
-  }
-  return u[0];
-}
-
 // Cluster all-reduce of NV <= 64 CTA partials already in xb (this CTA's slot):
 // one cluster barrier, then NV threads add the CS partials in rank order (the
 // same bits in every CTA) into out.
@@ -343,144 +318,81 @@ __device__ __forceinline__ void house_warp(double x, int lane, double& v, double
   v = lane == 0 ? 1.0 : x * (1.0 / (alpha - beta));
 }
 
-// Row access for one stage-2 task (rows q0 .. q0+m-1 of the band): S2Fast when
-// all of them sit in this CTA's shared memory (consecutive rows, plain shared
-// addressing), S2Gen otherwise (the next CTA's shared memory over DSMEM, or
-// the global spill rows).
-struct S2Gen {
-  double *rows, *rows_nx, *spill;
-  int q0, lo, hi, R, RS, cr;
-  __device__ __forceinline__ double* row(int i) const {
-    const int r = q0 + i;
-    const int owner = r < hi ? cr : cr + 1;
-    const int lr = r - owner * R;
-    if (lr < RS) return (r < hi ? rows : rows_nx) + (size_t)lr * S2_LDL;
-    return spill + ((size_t)owner * (R - RS) + (lr - RS)) * S2_LDL;
+// 32 broadcast doubles from shared memory into registers (16-byte loads), so
+// the compiler can issue them all before a phase's stores (with the loads
+// interleaved with stores to the band rows it cannot hoist them: possible alias)
+__device__ __forceinline__ void bcast32(const double* src, double (&r)[SB]) {
+#pragma unroll
+  for (int t = 0; t < SB; t += 2) {
+    const double2 q = *reinterpret_cast<const double2*>(src + t);
+    r[t] = q.x;
+    r[t + 1] = q.y;
   }
-};
+}
 
-// One bulge-chasing task (s, j) on rows q0 .. q0+m-1 (lane i <-> row q0+i):
-// j = 0 annihilates column s (T1), j > 0 right-applies the previous block's
-// reflector (vp, taup) to B = A[block j, block j-1] and annihilates its first
-// column (T2); then D = A[block j, block j] <- H D H (T3). The lane's rows of B
-// and D live in registers for the task.
-template <class Acc>
-__device__ __forceinline__ void s2_task(const Acc& acc, int j, int m, int lane, double vp, double taup, double* vs,
-                                        double* ws, double* zs, double& v, double& tau) {
-  const bool act = lane < m;
-  double* rp = acc.row(act ? lane : 0);
+// Rows q0 .. q0+m-1 of a task in at most two runs of consecutive rows at stride
+// S2_LDL: rows [0, h) at base, rows [h, m) at base2 (the next CTA's shared memory
+// over DSMEM, or the global spill rows). Lanes >= m are inactive (the last block
+// of a sweep).
+template <bool SEG, bool PART>
+__device__ __forceinline__ void s2_task_fast(double* base, double* base2, int h, int m_, int j, int lane, double vp,
+                                             double taup, double* vs, double* ws, double* zs, double& v, double& tau,
+                                             long long* ph) {
+  auto row = [&](int i) -> double* {
+    if constexpr (SEG) return i < h ? base + i * S2_LDL : base2 + (i - h) * S2_LDL;
+    return base + i * S2_LDL;
+  };
+  const int m = PART ? m_ : SB;  // PART: a short last block (lanes >= m inactive)
+  const bool act = !PART || lane < m;
+  double* rp = row(act ? lane : 0);
   double beta;
+  long long c0 = clock64(), c1 = c0, c2 = c0, c3 = c0;
   if (j == 0) {
     const double x = act ? rp[1 + lane] : 0.0;  // column s, rows q0 + lane
     house_warp(x, lane, v, tau, beta);
     if (act) rp[1 + lane] = lane == 0 ? beta : 0.0;
   } else {
-    // brow[jj] = B[lane][jj] = A[q0+lane][q0-SB+jj] = L[q0+lane][SB+lane-jj]
-    double brow[SB];
-#pragma unroll
-    for (int jj = 0; jj < SB; ++jj) brow[jj] = act ? rp[SB + lane - jj] : 0.0;
-    vs[lane] = vp;
-    __syncwarp();
-    double y0 = 0.0, y1 = 0.0;  // right-apply H_{j-1}: B <- B (I - taup vp vp^T)
-#pragma unroll
-    for (int jj = 0; jj < SB; jj += 2) {
-      y0 = fma(brow[jj], vs[jj], y0);
-      y1 = fma(brow[jj + 1], vs[jj + 1], y1);
-    }
-    const double ty = taup * (y0 + y1);
-#pragma unroll
-    for (int jj = 0; jj < SB; ++jj) brow[jj] = fma(-ty, vs[jj], brow[jj]);
-    house_warp(brow[0], lane, v, tau, beta);
-    // left-apply: z_jj = sum_i v_i B[i][jj] (a reduce-scatter over the lanes), B -= tau v z^T
-    const double z = rs_scaled(brow, v, lane);
-    zs[lane] = tau * z;
-    __syncwarp();
-#pragma unroll
-    for (int jj = 1; jj < SB; ++jj) brow[jj] = fma(-v, zs[jj], brow[jj]);
-    if (act) {
-      rp[SB + lane] = lane == 0 ? beta : 0.0;
-#pragma unroll
-      for (int jj = 1; jj < SB; ++jj) rp[SB + lane - jj] = brow[jj];
-    }
-  }
-  __syncwarp();
-  // D (m x m, lower in L[q0+i][i-c]): the lane's full symmetric row in registers
-  double drow[SB];
-#pragma unroll
-  for (int cc = 0; cc < SB; ++cc) {
-    double dv = 0.0;
-    if (act && cc < m) dv = cc <= lane ? rp[lane - cc] : acc.row(cc)[cc - lane];
-    drow[cc] = dv;
-  }
-  vs[lane] = v;
-  __syncwarp();
-  double p0 = 0.0, p1 = 0.0;
-#pragma unroll
-  for (int cc = 0; cc < SB; cc += 2) {
-    p0 = fma(drow[cc], vs[cc], p0);
-    p1 = fma(drow[cc + 1], vs[cc + 1], p1);
-  }
-  const double p = tau * (p0 + p1);
-  const double K = 0.5 * tau * wsum(p * v);
-  const double w = fma(-K, v, p);
-  ws[lane] = w;
-  __syncwarp();
-  if (act) {
-#pragma unroll
-    for (int cc = 0; cc < SB; ++cc)
-      if (cc <= lane) rp[lane - cc] = fma(-v, ws[cc], fma(-w, vs[cc], drow[cc]));
-  }
-}
-
-// Fast path of s2_task: m = 32 and every row in this CTA's shared memory at
-// base + i * S2_LDL, so every access is a shared load/store at a lane base
-// plus an immediate (row stride 65 doubles: column walks are conflict-free).
-__device__ __forceinline__ void s2_task_fast(double* base, int j, int lane, double vp, double taup, double* vs,
-                                             double* ws, double* zs, double& v, double& tau, long long* ph) {
-  double* rp = base + lane * S2_LDL;
-  double beta;
-  long long c0 = clock64(), c1 = c0, c2 = c0, c3 = c0;
-  if (j == 0) {
-    const double x = rp[1 + lane];  // column s, rows q0 + lane
-    house_warp(x, lane, v, tau, beta);
-    rp[1 + lane] = lane == 0 ? beta : 0.0;
-  } else {
     double brow[SB];  // B[lane][jj] = L[q0+lane][SB+lane-jj]
     double* bp = rp + SB + lane;
 #pragma unroll
-    for (int jj = 0; jj < SB; ++jj) brow[jj] = bp[-jj];
+    for (int jj = 0; jj < SB; ++jj) brow[jj] = act ? bp[-jj] : 0.0;
     vs[lane] = vp;
     __syncwarp();
+    double b32[SB];
+    bcast32(vs, b32);
     double y0 = 0.0, y1 = 0.0;
 #pragma unroll
     for (int jj = 0; jj < SB; jj += 2) {
-      y0 = fma(brow[jj], vs[jj], y0);
-      y1 = fma(brow[jj + 1], vs[jj + 1], y1);
+      y0 = fma(brow[jj], b32[jj], y0);
+      y1 = fma(brow[jj + 1], b32[jj + 1], y1);
     }
     const double ty = taup * (y0 + y1);
 #pragma unroll
     for (int jj = 0; jj < SB; ++jj) {
-      brow[jj] = fma(-ty, vs[jj], brow[jj]);
-      bp[-jj] = brow[jj];
+      brow[jj] = fma(-ty, b32[jj], brow[jj]);
+      if (act) bp[-jj] = brow[jj];
     }
     c1 = clock64();
     house_warp(brow[0], lane, v, tau, beta);
     c2 = clock64();
     ws[lane] = v;
     __syncwarp();
+    bcast32(ws, b32);
     // z_lane = sum_i v_i B[i][lane] = sum_i v_i L[q0+i][SB+i-lane]: column walk
-    const double* cp = base + SB - lane;
     double z0 = 0.0, z1 = 0.0;
 #pragma unroll
     for (int i = 0; i < SB; i += 2) {
-      z0 = fma(ws[i], cp[i * (S2_LDL + 1)], z0);
-      z1 = fma(ws[i + 1], cp[(i + 1) * (S2_LDL + 1)], z1);
+      if (i < m) z0 = fma(b32[i], row(i)[SB + i - lane], z0);
+      if (i + 1 < m) z1 = fma(b32[i + 1], row(i + 1)[SB + i + 1 - lane], z1);
     }
     zs[lane] = tau * (z0 + z1);
     __syncwarp();
-    bp[0] = lane == 0 ? beta : 0.0;
+    bcast32(zs, b32);
+    if (act) {
+      bp[0] = lane == 0 ? beta : 0.0;
 #pragma unroll
-    for (int jj = 1; jj < SB; ++jj) bp[-jj] = fma(-v, zs[jj], brow[jj]);
+      for (int jj = 1; jj < SB; ++jj) bp[-jj] = fma(-v, b32[jj], brow[jj]);
+    }
   }
   __syncwarp();
   c3 = clock64();
@@ -490,26 +402,32 @@ __device__ __forceinline__ void s2_task_fast(double* base, int j, int lane, doub
   const double* lp = rp + lane;
 #pragma unroll
   for (int cc = 0; cc < SB; ++cc) {
-    const double* ad = cc <= lane ? lp - cc : rp + (cc - lane) * (S2_LDL + 1);
-    drow[cc] = *ad;
+    const double* ad = cc <= lane ? lp - cc : row(cc) + (cc - lane);
+    drow[cc] = (act && cc < m) ? *ad : 0.0;
   }
   vs[lane] = v;
   __syncwarp();
+  double v32[SB];
+  bcast32(vs, v32);
   double p0 = 0.0, p1 = 0.0;
 #pragma unroll
   for (int cc = 0; cc < SB; cc += 2) {
-    p0 = fma(drow[cc], vs[cc], p0);
-    p1 = fma(drow[cc + 1], vs[cc + 1], p1);
+    p0 = fma(drow[cc], v32[cc], p0);
+    p1 = fma(drow[cc + 1], v32[cc + 1], p1);
   }
   const double p = tau * (p0 + p1);
   const double K = 0.5 * tau * wsum(p * v);
   const double w = fma(-K, v, p);
   ws[lane] = w;
   __syncwarp();
+  double w32[SB];
+  bcast32(ws, w32);
   double* up = rp + lane;
+  if (act) {
 #pragma unroll
-  for (int cc = 0; cc < SB; ++cc)
-    if (cc <= lane) up[-cc] = fma(-v, ws[cc], fma(-w, vs[cc], drow[cc]));
+    for (int cc = 0; cc < SB; ++cc)
+      if (cc <= lane) up[-cc] = fma(-v, w32[cc], fma(-w, v32[cc], drow[cc]));
+  }
   __syncwarp();
   if (ph && j > 0) {
     const long long c4 = clock64();
@@ -594,11 +512,20 @@ __global__ void __launch_bounds__(S2_W * 32, 1) k_sb2st(const S2Args a) {
       pw += t1 - t0;
       const int m = min(SB, n - q0);
       double v, tau;
-      if (m == SB && q0 + m <= lo + min(RS, hi - lo)) {  // every row of the block in this CTA's shared memory
-        s2_task_fast(rows + (size_t)(q0 - lo) * S2_LDL, j, lane, vp, taup, vs, ws, zs, v, tau, a.prof ? ph : nullptr);
+      // rows q0 .. q0+m-1 as one or two runs of consecutive rows: this CTA's
+      // shared rows [lo, lo+RS), its spill rows [lo+RS, hi), the next CTA's rows
+      const int lsm = lo + min(RS, hi - lo);  // end of this CTA's shared-memory rows
+      double* b1 = q0 < lsm ? rows + (size_t)(q0 - lo) * S2_LDL
+                            : a.spill + ((size_t)cr * (R - RS) + (q0 - lsm)) * S2_LDL;
+      const int e1 = q0 < lsm ? lsm : hi;  // end of the first run
+      long long* php = a.prof ? ph : nullptr;
+      if (q0 + m <= e1) {
+        if (m == SB) s2_task_fast<false, false>(b1, b1, m, m, j, lane, vp, taup, vs, ws, zs, v, tau, php);
+        else s2_task_fast<false, true>(b1, b1, m, m, j, lane, vp, taup, vs, ws, zs, v, tau, php);
       } else {
-        S2Gen acc{rows, rows_nx, a.spill, q0, lo, hi, R, RS, cr};
-        s2_task(acc, j, m, lane, vp, taup, vs, ws, zs, v, tau);
+        double* b2 = e1 == lsm && lsm < hi ? a.spill + (size_t)cr * (R - RS) * S2_LDL : rows_nx;
+        if (m == SB) s2_task_fast<true, false>(b1, b2, e1 - q0, m, j, lane, vp, taup, vs, ws, zs, v, tau, php);
+        else s2_task_fast<true, true>(b1, b2, e1 - q0, m, j, lane, vp, taup, vs, ws, zs, v, tau, php);
       }
       // hand-off to the next CTA, then publish progress (release at cluster scope)
       const int q0n = q0 + SB;
@@ -686,7 +613,8 @@ void panel_qr_cs(Ctx& c, const PanelArgs& pa) {
 constexpr int IV_W = 4;                 // warps (eigenvalues) per block
 constexpr int IV_R = SB + 1;            // window rows
 constexpr int IV_C = 2 * SB + 1;        // window columns = U row length
-constexpr int IV_SMEM_WARP = IV_R * IV_C + 32 + IV_R + IV_C;
+constexpr int IV_WIN = (IV_R * IV_C + 1) / 2 * 2;  // window, rounded to 16 bytes
+constexpr int IV_SMEM_WARP = (IV_WIN + 32 + IV_R + IV_C + 1) / 2 * 2;  // per-warp base stays 16-byte aligned
 
 __device__ __forceinline__ double start_entry(int64_t vi, int64_t i) {
   uint64_t h = (uint64_t)vi * 0x9E3779B97F4A7C15ull ^ ((uint64_t)i + 0x632BE59BD9B4E019ull);
@@ -724,7 +652,7 @@ __global__ void __launch_bounds__(IV_W * 32) k_band_invit(const double* __restri
   const int64_t vi = (int64_t)blockIdx.x * IV_W + warp;
   if (vi >= k) return;
   double* W = smi + (size_t)warp * IV_SMEM_WARP;  // [row % IV_R][col % IV_C]
-  double* mult = W + IV_R * IV_C;
+  double* mult = W + IV_WIN;
   double* yw = mult + 32;                         // forward window (IV_R)
   double* xw = yw + IV_R;                         // back window (IV_C)
   const double sigma = vals[vi];
@@ -734,10 +662,13 @@ __global__ void __launch_bounds__(IV_W * 32) k_band_invit(const double* __restri
   int* piv = pb + (size_t)vi * n;
   double* y = yb + (size_t)vi * n;
   double* x = z + (size_t)vi * n;
-  auto bval = [&](int r, int cc) -> double {  // (B - sigma I)[r][cc], zero outside the band / matrix
+  auto braw = [&](int r, int cc) -> double {  // B[r][cc], zero outside the band / matrix
     if (r >= n || cc < 0 || cc >= n || cc - r > SB || r - cc > SB) return 0.0;
-    const double v = __ldg(band + (size_t)r * IV_C + (cc - r + SB));
-    return cc == r ? v - sigma : v;
+    return __ldg(band + (size_t)r * IV_C + (cc - r + SB));
+  };
+  auto bval = [&](int r, int cc) -> double {  // (B - sigma I)[r][cc]
+    const double v = braw(r, cc);
+    return cc == r && r < n ? v - sigma : v;
   };
   for (int rr = 0; rr < IV_R; ++rr)
     for (int cc = lane; cc < IV_C; cc += 32) W[rr * IV_C + cc] = bval(rr, cc);
@@ -745,12 +676,14 @@ __global__ void __launch_bounds__(IV_W * 32) k_band_invit(const double* __restri
   // ---- LU with partial pivoting; the row entering the window (i + b + 1 at
   // the end of step i) is loaded two steps ahead into registers
   double nr[2][3];
+  // raw band values (the shift is applied when the row enters the window, so
+  // no arithmetic waits on these loads in the step that issues them)
 #pragma unroll
   for (int q = 0; q < 2; ++q)
 #pragma unroll
     for (int u = 0; u < 3; ++u) {
       const int off = lane + 32 * u;
-      nr[q][u] = (u < 2 || lane == 0) ? bval(IV_R + q, q + 1 + off) : 0.0;
+      nr[q][u] = (u < 2 || lane == 0) ? braw(IV_R + q, q + 1 + off) : 0.0;
     }
   for (int i = 0; i < n; ++i) {
     const int nw = min(IV_R, n - i);
@@ -767,7 +700,7 @@ __global__ void __launch_bounds__(IV_W * 32) k_band_invit(const double* __restri
 #pragma unroll
     for (int u = 0; u < 3; ++u) {
       const int off = lane + 32 * u;
-      nn[u] = (u < 2 || lane == 0) ? bval(i + IV_R + 2, i + 3 + off) : 0.0;
+      nn[u] = (u < 2 || lane == 0) ? braw(i + IV_R + 2, i + 3 + off) : 0.0;
     }
     for (int o = 16; o > 0; o >>= 1) {
       const double oc = __shfl_xor_sync(FULL, cand, o);
@@ -786,18 +719,28 @@ __global__ void __launch_bounds__(IV_W * 32) k_band_invit(const double* __restri
     if (pv == 0.0) pv = tiny;
     double ml = 0.0;
     if (lane < nw - 1) ml = W[((i + 1 + lane) % IV_R) * IV_C + ci] / pv;
-    mult[lane] = ml;
     L[(size_t)i * SB + lane] = ml;
     if (lane == 0) piv[i] = pr;
     __syncwarp();
-    for (int off = 1 + lane; off < IV_C; off += 32) {
-      const int cc = i + off;
-      if (cc >= n) break;
-      const double u = prow[cc % IV_C];
-      for (int r = 0; r < nw - 1; ++r) {
-        double* wp = W + ((i + 1 + r) % IV_R) * IV_C + cc % IV_C;
-        *wp = fma(-mult[r], u, *wp);
+    // Row-wise elimination: lane l owns window row i+1+l and updates all its 65
+    // column slots against the pivot row at static offsets (column c sits in
+    // slot c mod 65, the same in every row), in chunks whose loads all precede
+    // their stores (the compiler cannot hoist loads past possibly aliasing
+    // stores). Slot i (column i + 65 from now on) is then zeroed.
+    if (lane < nw - 1) {
+      double* wr = W + ((i + 1 + lane) % IV_R) * IV_C;
+      constexpr int CH = 22;
+#pragma unroll
+      for (int c0 = 0; c0 < IV_C; c0 += CH) {
+        double ow[CH], pw[CH];
+#pragma unroll
+        for (int t = 0; t < CH; ++t)
+          if (c0 + t < IV_C) { ow[t] = wr[c0 + t]; pw[t] = prow[c0 + t]; }
+#pragma unroll
+        for (int t = 0; t < CH; ++t)
+          if (c0 + t < IV_C) wr[c0 + t] = fma(-ml, pw[t], ow[t]);
       }
+      wr[ci] = 0.0;
     }
     for (int off = lane; off < IV_C; off += 32) {
       const int cc = i + off;
@@ -805,14 +748,16 @@ __global__ void __launch_bounds__(IV_W * 32) k_band_invit(const double* __restri
     }
     __syncwarp();
     // the next row (i + b + 1) takes row i's slot; column i + 2b + 1 takes column i's
+    const int rn = i + IV_R;
 #pragma unroll
     for (int u = 0; u < 3; ++u) {
       const int off = lane + 32 * u;
-      if (u < 2 || lane == 0) prow[(i + 1 + off) % IV_C] = nr[0][u];
+      // the entering row i + b + 1 meets the diagonal at offset 32 (lane 0, u = 1)
+      if (u < 2 || lane == 0)
+        prow[(i + 1 + off) % IV_C] = (u == 1 && lane == 0 && rn < n) ? nr[0][u] - sigma : nr[0][u];
       nr[0][u] = nr[1][u];
       nr[1][u] = nn[u];
     }
-    if (lane < IV_R - 1) W[((i + 1 + lane) % IV_R) * IV_C + ci] = 0.0;
     __syncwarp();
   }
   // ---- two solves: x <- U^-1 L^-1 P y, y = start, then y = x / |x|.
@@ -870,15 +815,15 @@ __global__ void __launch_bounds__(IV_W * 32) k_band_invit(const double* __restri
     __syncwarp();
     double ss = 0.0;
     double u0c[PD], u1c[PD], rc[PD], ycb[PD];
-    auto uld = [&](int i, double& a0, double& a1, double& rinv, double& yv) {
+    auto uld = [&](int i, double& a0, double& a1, double& dg, double& yv) {
       if (i >= 0) {
         const double* ur = U + (size_t)i * IV_C;
         a0 = ur[1 + lane];
         a1 = ur[33 + lane];
-        rinv = 1.0 / ur[0];
+        dg = ur[0];
         yv = y[i];
       } else {
-        a0 = a1 = 0.0; rinv = 0.0; yv = 0.0;
+        a0 = a1 = 0.0; dg = 1.0; yv = 0.0;
       }
     };
     // y[] was written by lane 0 during the forward pass: make it visible to the warp
@@ -887,6 +832,8 @@ __global__ void __launch_bounds__(IV_W * 32) k_band_invit(const double* __restri
     for (int u = 0; u < PD; ++u) uld(n - 1 - u, u0c[u], u1c[u], rc[u], ycb[u]);
     for (int i0 = n - 1; i0 >= 0; i0 -= PD) {
       double u0n[PD], u1n[PD], rn[PD], ynb[PD];
+#pragma unroll
+      for (int u = 0; u < PD; ++u) rc[u] = 1.0 / rc[u];  // this chunk's pivots arrived a chunk ago
 #pragma unroll
       for (int u = 0; u < PD; ++u) uld(i0 - PD - u, u0n[u], u1n[u], rn[u], ynb[u]);
 #pragma unroll
@@ -1043,7 +990,9 @@ constexpr int S2_MAXRS = (int)((227 * 1024 - S2_FIXED) / (sizeof(double) * S2_LD
 template <int CS>
 void sb2st_cs(Ctx& c, const double* band, int n, double* d, double* e) {
   const int R = (n + CS - 1) / CS;
-  const int RS = std::min(R, S2_MAXRS);
+  // rows kept in shared memory; a spill region, when needed, holds >= SB rows so
+  // a task's 32 rows never span more than two runs (smem | spill | next CTA)
+  const int RS = R <= S2_MAXRS ? R : std::min(S2_MAXRS, R - SB);
   const size_t smem = S2_FIXED + sizeof(double) * (size_t)RS * S2_LDL;
   const size_t mk = c.arena.mark();
   double* spill = R > RS ? alloc<double>(c, (size_t)CS * (R - RS) * S2_LDL) : nullptr;

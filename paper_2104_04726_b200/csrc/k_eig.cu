@@ -1917,7 +1917,7 @@ static void bisect_top(Ctx& c, const double* d, const double* e, int64_t n, int6
 // trailing updates) -> tridiagonal (cluster bulge chasing) -> eigenvalues by
 // multisection -> eigenvectors of the band by inverse iteration -> stage-1
 // reflectors back-applied in compact-WY panels -> Newton-Schulz.
-// Default for n > 4000 (C5's n = 4320 and 7680 Grams); TMB_EIG_2STAGE=1 forces it
+// Default for n > 4600 (C5's n = 7680 Gram); TMB_EIG_2STAGE=1 forces it
 // (tests, A/B runs), =0 disables it. Returns false,
 // with nothing written but scratch, when the vectors of a tight eigenvalue
 // cluster came out (nearly) parallel: the caller then runs the one-stage path,
@@ -1928,10 +1928,10 @@ static bool two_stage_for(int64_t n) {
     return s ? std::atoi(s) : -1;
   }();
   if (n < 4 * SBR_B || mode == 0) return false;
-  // measured crossover (scripts/gpu_s3_ab.sh, two-stage vs one-stage): n = 7680
-  // 239 vs 410 ms (k = 960), n = 4320 92 vs 95 ms (k = 540), n = 3840 82 vs 71 ms
-  // (k = 960), n = 2160 40 vs 19 ms
-  return mode == 1 || n > 4000;
+  // measured crossover (scripts/gpu_s3_ab.sh, two-stage vs one-stage with the
+  // shared-memory hand-off): n = 7680 239 vs 402 ms (k = 960), n = 5000 114 vs
+  // 131 ms (k = 600), n = 4320 92 vs 88 ms (k = 540), n = 3840 82 vs 64 ms (k = 960)
+  return mode == 1 || n > 4600;
 }
 
 static bool eig_two_stage(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs, double* vals) {
@@ -2039,10 +2039,37 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
   {
     Timed timed(c, TAG_SYTRD, 4.0 / 3.0 * (double)n * n * n);  // dsytrd flop count
     static const bool rows_off = std::getenv("TMB_SYTRD_COLS") != nullptr;  // A/B: force the column kernel
+    bool handed = false;
     if (K0 > 0 && (rows_off || !sytrd_rows(c, A, n, K0, d, e, tau, hv, pbuf))) {
-      ta.k_begin = sytrd_lazy_panels(c, A, n, std::min<int64_t>(K0, n - 3), d, e, tau, hv);
+      // n > 2048: lazy panels while the trailing matrix exceeds L2, the column
+      // kernel down to trailing size kHandSmem, then the shared-memory kernel on
+      // the trailing block (its Gram slice fits the 148 SMs' shared memory; the
+      // column kernel re-streams it from L2 every step). TMB_SYTRD_HANDOFF=0: off.
+      static const bool hand_off = [] {
+        const char* s = std::getenv("TMB_SYTRD_HANDOFF");
+        return !(s && std::atoi(s) == 0);
+      }();
+      constexpr int64_t kHandSmem = 2000;
+      const int64_t km = n - kHandSmem;
+      const bool hand = hand_off && tail1 && !rows_off && km > 0 && km < K0;
+      ta.k_begin = sytrd_lazy_panels(c, A, n, std::min<int64_t>(hand ? km : K0, n - 3), d, e, tau, hv);
+      if (hand) ta.k_end = std::max(km, ta.k_begin);
       TMB_CUDA(cudaLaunchCooperativeKernel(kern, blocks, TRD_THREADS, args, smem, c.stream));
       LAUNCHED("k_sytrd");
+      if (hand) {
+        // the column kernel stopped after step k1-1: reflector k1 (hv column k1, tau, d, e)
+        // is known and rows/columns > k1 are updated through step k1-1 -- the shared-memory
+        // kernel resumes from there on the block starting at k1
+        const int64_t k1 = ta.k_end, n1 = n - k1;
+        TMB_CUDA(cudaMemsetAsync(hv + n * (k1 + 1), 0, sizeof(double) * n * (n - k1 - 1), c.stream));
+        handed = sytrd_smem(c, A + k1 + n * k1, n1, K0 - k1, d + k1, e + k1, tau + k1, hv + k1 + n * k1, pbuf, n, 1);
+        if (!handed) {  // did not fit after all: the column kernel finishes from k1
+          ta.k_begin = k1;
+          ta.k_end = K0;
+          TMB_CUDA(cudaLaunchCooperativeKernel(kern, blocks, TRD_THREADS, args, smem, c.stream));
+          LAUNCHED("k_sytrd");
+        }
+      }
     }
     if (tail1) sytrd_tail1(c, A, n, K0, d, e, tau, hv);
     else if (K0 < n) sytrd_tail(c, A, n, K0, d, e, tau, hv);

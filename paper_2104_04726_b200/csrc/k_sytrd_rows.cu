@@ -32,6 +32,9 @@ struct RowArgs {
   int64_t n, k_end;
   double* d; double* e; double* tau; double* hv;
   double* pbuf;  // 2 x n: p_k by step parity
+  int64_t ld = 0;  // k_sytrd_smem: leading dimension of A and hv (0: n) -- a trailing block of a larger matrix
+  int resume = 0;  // k_sytrd_smem: reflector 0 (hv column 0, tau[0]) and d[0], e[0] already computed by
+                   // the kernel that ran the earlier steps; A holds rows/columns >= 1 updated through them
 };
 
 __device__ __forceinline__ double frcp(double b) {
@@ -329,6 +332,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
   cg::grid_group grid = cg::this_grid();
   const int N = (int)a.n;
   const int64_t n = a.n;
+  const int64_t ld = a.ld ? a.ld : a.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NB = gridDim.x, b = blockIdx.x;
   double* A = a.A;
@@ -349,7 +353,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
     qi[u] = (i >= jb && i < N && (i - jb) % NB == 0) ? (i - jb) / NB : -1;
   }
   for (int q = 0; q < nown; ++q) {
-    const double* src = A + n * (jb + (int64_t)NB * q);
+    const double* src = A + ld * (jb + (int64_t)NB * q);
     for (int i = tid; i < N; i += NT) cols[q * N + i] = src[i];
   }
 
@@ -378,7 +382,16 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
     if (qi[u] >= 0) vo[qi[u]] = vr[u];
     if (i == 2) piv[0] = vr[u];
   }
-  if (b == 0) {
+  if (a.resume) {  // continue a reduction: v_0 and tau_0 come from the earlier kernel
+    tau_k = a.tau[0];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int i = tid + NT * u;
+      vr[u] = (i >= 1 && i < N) ? a.hv[i] : 0.0;
+      if (qi[u] >= 0) vo[qi[u]] = vr[u];
+      if (i == 2) piv[0] = vr[u];
+    }
+  } else if (b == 0) {
     if (tid == 0) { a.d[0] = A[0]; a.e[0] = beta; a.tau[0] = tau_k; }
 #pragma unroll
     for (int u = 0; u < RPT; ++u) {
@@ -420,9 +433,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
       const int i = tid + NT * u;
       const bool live = i >= c1 && i < N;
       pp[u] = live ? pb[i] : 0.0;
-      xa[u] = live ? A[i + n * c1] : 0.0;
+      xa[u] = live ? A[i + ld * c1] : 0.0;
     }
-    const double p_c1 = pb[c1], p_k2 = pb[k + 2], a_k2 = A[(k + 2) + n * c1];
+    const double p_c1 = pb[c1], p_k2 = pb[k + 2], a_k2 = A[(k + 2) + ld * c1];
     double pv = 0.0;
 #pragma unroll
     for (int u = 0; u < RPT; ++u) pv = fma(pp[u], vr[u], pv);
@@ -447,7 +460,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
           if (i == N - 2) a.d[N - 2] = xa[u];
           if (i == N - 1) {
             a.e[N - 2] = xa[u];
-            a.d[N - 1] = A[(n - 1) + n * (n - 1)] - 2.0 * vr[u] * wr[u];
+            a.d[N - 1] = A[(n - 1) + ld * (n - 1)] - 2.0 * vr[u] * wr[u];
             a.tau[N - 2] = 0.0;
           }
         }
@@ -484,7 +497,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
     }
     if (b == 0) {
       if (tid == 0) { a.e[c1] = beta; a.tau[c1] = tau_n; }
-      double* h = a.hv + n * c1;
+      double* h = a.hv + ld * c1;
 #pragma unroll
       for (int u = 0; u < RPT; ++u) {
         const int i = tid + NT * u;
@@ -535,12 +548,12 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
     }
     // publish the next pivot column (and, before the last step, the last diagonal)
     if (qpub >= q0 && qpub >= 0 && qpub < nown) {
-      double* gq = A + n * k2;
+      double* gq = A + ld * k2;
 #pragma unroll
       for (int u = 0; u < RPT; ++u)
         if (lv[u]) gq[tid + NT * u] = cols[qpub * N + tid + NT * u];
     }
-    if (qlast >= 0 && qlast < nown && tid == (N - 1) % NT) A[(n - 1) + n * (n - 1)] = cols[qlast * N + N - 1];
+    if (qlast >= 0 && qlast < nown && tid == (N - 1) % NT) A[(n - 1) + ld * (n - 1)] = cols[qlast * N + N - 1];
     SM_T(6);
     __syncthreads();
     SM_T(7);
@@ -578,7 +591,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
     for (int q = 0; q < nown; ++q) {
       const int64_t j = jb + (int64_t)NB * q;
       if (j <= k) continue;
-      double* dst = A + n * j;
+      double* dst = A + ld * j;
       for (int i = (int)k + 1 + tid; i < N; i += NT) dst[i] = cols[q * N + i];
     }
   }
@@ -589,7 +602,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
 
 // Shared-memory-resident launch; false if the owned columns do not fit.
 bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* e, double* tau, double* hv,
-                double* pbuf) {
+                double* pbuf, int64_t ld, int resume) {
   static const int nt_env = [] {
     const char* s = std::getenv("TMB_SMEM_NT");  // A/B: 256 (2 blocks/SM) or 512 (1 block/SM)
     return s ? std::atoi(s) : 0;
@@ -633,7 +646,7 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
     prof = alloc<long long>(c, 80);
     TMB_CUDA(cudaMemsetAsync(prof, 0, sizeof(long long) * 80, c.stream));
   }
-  RowArgs ra{A, n, k_end, d, e, tau, hv, pbuf};
+  RowArgs ra{A, n, k_end, d, e, tau, hv, pbuf, ld, resume};
   void* args[] = {&ra, (void*)&qmax, &prof};
   TMB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, nb, nt, args, smem, c.stream));
   c.launches++;
@@ -663,7 +676,7 @@ bool sytrd_rows(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
   static const bool smem_off = std::getenv("TMB_SYTRD_L2") != nullptr;  // A/B: force the L2-streaming variant
   // measured (scripts/ab_smem.sh): n=1920 8.8 vs 11.9 ms, n=1080 4.4 vs 5.0 ms,
   // n=500 1.75 vs 1.65 ms (L2 variant keeps small n)
-  if (!smem_off && n > 600 && sytrd_smem(c, A, n, k_end, d, e, tau, hv, pbuf)) return true;
+  if (!smem_off && n > 600 && sytrd_smem(c, A, n, k_end, d, e, tau, hv, pbuf, n, 0)) return true;
   static const int cb_env = [] {
     const char* s = std::getenv("TMB_ROWS_CB");  // A/B: columns per load batch
     return s ? std::atoi(s) : 0;

@@ -157,6 +157,13 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
 // false if n is out of its range.
 bool sytrd_rows(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* e, double* tau, double* hv,
                 double* pbuf);
+// Shared-memory-resident tridiagonalisation of an n x n symmetric block stored with leading
+// dimension ld (d, e, tau, hv offset to the block; hv with the same ld); steps 0 .. k_end-1,
+// the rest left in A for a tail kernel. resume: reflector 0 (hv column 0, tau[0], d[0], e[0])
+// was computed by the kernel that ran the earlier steps (the column kernel stopped there).
+// False if the block's columns do not fit shared memory.
+bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* e, double* tau, double* hv,
+                double* pbuf, int64_t ld, int resume);
 // Cluster-resident tridiagonalisation of the trailing block from step K0 (k_sytrd_tail.cu).
 int64_t sytrd_tail_capacity(Ctx& c);
 void sytrd_tail(Ctx& c, double* A, int64_t n, int64_t K0, double* d, double* e, double* tau, double* hv);

@@ -334,7 +334,7 @@ __device__ __forceinline__ void bcast32(const double* src, double (&r)[SB]) {
 // S2_LDL: rows [0, h) at base, rows [h, m) at base2 (the next CTA's shared memory
 // over DSMEM, or the global spill rows). Lanes >= m are inactive (the last block
 // of a sweep).
-template <bool SEG, bool PART>
+template <bool SEG, bool PART, bool PROF>
 __device__ __forceinline__ void s2_task_fast(double* base, double* base2, int h, int m_, int j, int lane, double vp,
                                              double taup, double* vs, double* ws, double* zs, double& v, double& tau,
                                              long long* ph) {
@@ -346,7 +346,8 @@ __device__ __forceinline__ void s2_task_fast(double* base, double* base2, int h,
   const bool act = !PART || lane < m;
   double* rp = row(act ? lane : 0);
   double beta;
-  long long c0 = clock64(), c1 = c0, c2 = c0, c3 = c0;
+  long long c0 = 0, c1 = 0, c2 = 0, c3 = 0;  // TMB_S2_PROF phase clocks
+  if constexpr (PROF) c0 = c1 = c2 = c3 = clock64();
   if (j == 0) {
     const double x = act ? rp[1 + lane] : 0.0;  // column s, rows q0 + lane
     house_warp(x, lane, v, tau, beta);
@@ -372,9 +373,9 @@ __device__ __forceinline__ void s2_task_fast(double* base, double* base2, int h,
       brow[jj] = fma(-ty, b32[jj], brow[jj]);
       if (act) bp[-jj] = brow[jj];
     }
-    c1 = clock64();
+    if constexpr (PROF) c1 = clock64();
     house_warp(brow[0], lane, v, tau, beta);
-    c2 = clock64();
+    if constexpr (PROF) c2 = clock64();
     ws[lane] = v;
     __syncwarp();
     bcast32(ws, b32);
@@ -395,7 +396,7 @@ __device__ __forceinline__ void s2_task_fast(double* base, double* base2, int h,
     }
   }
   __syncwarp();
-  c3 = clock64();
+  if constexpr (PROF) c3 = clock64();
   // D: the lane's full symmetric row; D[lane][c] = L[q0+lane][lane-c] (c <= lane)
   // or L[q0+c][c-lane] = rp[(c - lane) * (S2_LDL + 1)] (c > lane)
   double drow[SB];
@@ -429,13 +430,13 @@ __device__ __forceinline__ void s2_task_fast(double* base, double* base2, int h,
       if (cc <= lane) up[-cc] = fma(-v, w32[cc], fma(-w, v32[cc], drow[cc]));
   }
   __syncwarp();
-  if (ph && j > 0) {
+  if (PROF && j > 0) {
     const long long c4 = clock64();
     ph[0] += c1 - c0; ph[1] += c2 - c1; ph[2] += c3 - c2; ph[3] += c4 - c3; ph[4] += 1;
   }
 }
 
-template <int CS>
+template <int CS, bool PROF>
 __global__ void __launch_bounds__(S2_W * 32, 1) k_sb2st(const S2Args a) {
   extern __shared__ __align__(16) double sm[];
   cg::cluster_group cl = cg::this_cluster();
@@ -492,9 +493,9 @@ __global__ void __launch_bounds__(S2_W * 32, 1) k_sb2st(const S2Args a) {
     if (s + 1 + jst * SB >= hi) continue;
     double vp = 0.0, taup = 0.0;
     if (jst > 0) {  // reflector of (s, jst - 1) from the previous CTA
-      const long long t0 = clock64();
+      const long long t0 = PROF ? clock64() : 0;
       wait_for(s, jst, true);
-      pw += clock64() - t0;
+      if constexpr (PROF) pw += clock64() - t0;
       vp = hbox[(s % S2_NS) * 33 + lane];
       taup = hbox[(s % S2_NS) * 33 + 32];
     }
@@ -502,13 +503,13 @@ __global__ void __launch_bounds__(S2_W * 32, 1) k_sb2st(const S2Args a) {
     for (int j = jst;; ++j) {
       const int q0 = s + 1 + j * SB;
       if (q0 >= hi) break;
-      const long long t0 = clock64();
+      const long long t0 = PROF ? clock64() : 0;
       if (s > 0) {
         // (s-1, jd) ran on this CTA (CTA scope) or on the next one (cluster scope)
         const int jd = min(j + 1, jlast_prev);
         wait_for(s - 1, jd + 1, s + jd * SB >= hi);
       }
-      const long long t1 = clock64();
+      const long long t1 = PROF ? clock64() : 0;
       pw += t1 - t0;
       const int m = min(SB, n - q0);
       double v, tau;
@@ -518,14 +519,14 @@ __global__ void __launch_bounds__(S2_W * 32, 1) k_sb2st(const S2Args a) {
       double* b1 = q0 < lsm ? rows + (size_t)(q0 - lo) * S2_LDL
                             : a.spill + ((size_t)cr * (R - RS) + (q0 - lsm)) * S2_LDL;
       const int e1 = q0 < lsm ? lsm : hi;  // end of the first run
-      long long* php = a.prof ? ph : nullptr;
+      long long* php = ph;
       if (q0 + m <= e1) {
-        if (m == SB) s2_task_fast<false, false>(b1, b1, m, m, j, lane, vp, taup, vs, ws, zs, v, tau, php);
-        else s2_task_fast<false, true>(b1, b1, m, m, j, lane, vp, taup, vs, ws, zs, v, tau, php);
+        if (m == SB) s2_task_fast<false, false, PROF>(b1, b1, m, m, j, lane, vp, taup, vs, ws, zs, v, tau, php);
+        else s2_task_fast<false, true, PROF>(b1, b1, m, m, j, lane, vp, taup, vs, ws, zs, v, tau, php);
       } else {
         double* b2 = e1 == lsm && lsm < hi ? a.spill + (size_t)cr * (R - RS) * S2_LDL : rows_nx;
-        if (m == SB) s2_task_fast<true, false>(b1, b2, e1 - q0, m, j, lane, vp, taup, vs, ws, zs, v, tau, php);
-        else s2_task_fast<true, true>(b1, b2, e1 - q0, m, j, lane, vp, taup, vs, ws, zs, v, tau, php);
+        if (m == SB) s2_task_fast<true, false, PROF>(b1, b2, e1 - q0, m, j, lane, vp, taup, vs, ws, zs, v, tau, php);
+        else s2_task_fast<true, true, PROF>(b1, b2, e1 - q0, m, j, lane, vp, taup, vs, ws, zs, v, tau, php);
       }
       // hand-off to the next CTA, then publish progress (release at cluster scope)
       const int q0n = q0 + SB;
@@ -544,11 +545,11 @@ __global__ void __launch_bounds__(S2_W * 32, 1) k_sb2st(const S2Args a) {
       }
       vp = v;
       taup = tau;
-      pt += clock64() - t1;
+      if constexpr (PROF) pt += clock64() - t1;
       ++pn;
     }
   }
-  if (a.prof && lane == 0) {
+  if (PROF && lane == 0) {
     long long* q = a.prof + 8 * (blockIdx.x * S2_W + warp);
     q[0] = pw; q[1] = pt; q[2] = pn;
     for (int t = 0; t < 5; ++t) q[3 + t] = ph[t];
@@ -996,9 +997,10 @@ void sb2st_cs(Ctx& c, const double* band, int n, double* d, double* e) {
   const size_t smem = S2_FIXED + sizeof(double) * (size_t)RS * S2_LDL;
   const size_t mk = c.arena.mark();
   double* spill = R > RS ? alloc<double>(c, (size_t)CS * (R - RS) * S2_LDL) : nullptr;
-  set_smem_attr(c, (const void*)k_sb2st<CS>, smem);
-  if (CS > 8) allow_cluster16(c, (const void*)k_sb2st<CS>);
   static const bool prof_on = std::getenv("TMB_S2_PROF") != nullptr;
+  const void* kfn = prof_on ? (const void*)k_sb2st<CS, true> : (const void*)k_sb2st<CS, false>;
+  set_smem_attr(c, kfn, smem);
+  if (CS > 8) allow_cluster16(c, kfn);
   long long* prof = nullptr;
   if (prof_on) {
     prof = alloc<long long>(c, (size_t)CS * S2_W * 8);
@@ -1006,7 +1008,8 @@ void sb2st_cs(Ctx& c, const double* band, int n, double* d, double* e) {
   }
   S2Args a{band, n, R, RS, spill, d, e, prof};
   void* args[] = {&a};
-  launch_cluster(c, k_sb2st<CS>, CS, dim3(CS), S2_W * 32, smem, args);
+  if (prof_on) launch_cluster(c, k_sb2st<CS, true>, CS, dim3(CS), S2_W * 32, smem, args);
+  else launch_cluster(c, k_sb2st<CS, false>, CS, dim3(CS), S2_W * 32, smem, args);
   LAUNCHED("k_sb2st");
   if (prof) {
     std::vector<long long> h((size_t)CS * S2_W * 8);

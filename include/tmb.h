@@ -152,7 +152,8 @@ int tmb_leading_eigvecs(tmb_ctx* ctx, const double* g_dev, int64_t n, int64_t k,
 /* The tridiagonal form T = Q^T g Q behind leading_eigvecs for large n (the
  * two-stage reduction: dense -> band of half-bandwidth 32 -> tridiagonal; the
  * reference reaches the same T inside eigh, tensor.py:195). d: n diagonal,
- * e: n-1 subdiagonal entries (device). n >= 3. */
+ * e: n-1 subdiagonal entries (device). 3 <= n <= 8000 (the band of stage 2 lives in one
+ * 16-CTA thread-block cluster). */
 int tmb_tridiagonalize(tmb_ctx* ctx, const double* g_dev, int64_t n, double* d_dev, double* e_dev);
 /* fro_norm^2 (tensor.py:212-214), deterministic fp64 reduction; host result. */
 int tmb_sumsq(tmb_ctx* ctx, const void* x_dev, int dtype, int64_t n, double* out_host);

@@ -272,7 +272,7 @@ int tmb_leading_eigvecs(tmb_ctx* ctx, const double* g, int64_t n, int64_t k, dou
 
 int tmb_tridiagonalize(tmb_ctx* ctx, const double* g, int64_t n, double* d, double* e) {
   return guard(ctx, [&](tmb::Ctx& c) {
-    if (n < 3) throw Error(TMB_EINVAL, "tridiagonalize: n must be >= 3");
+    if (n < 3 || n > 8000) throw Error(TMB_EINVAL, "tridiagonalize: n must be in [3, 8000]");
     const size_t mk = c.arena.mark();
     double* A = tmb::alloc<double>(c, (size_t)n * n);
     double* hv = tmb::alloc<double>(c, (size_t)n * n);

@@ -1922,12 +1922,16 @@ static void bisect_top(Ctx& c, const double* d, const double* e, int64_t n, int6
 // with nothing written but scratch, when the vectors of a tight eigenvalue
 // cluster came out (nearly) parallel: the caller then runs the one-stage path,
 // whose cluster repair works on the tridiagonal matrix.
-static bool two_stage_for(int64_t n) {
+static bool two_stage_for(int64_t n, int64_t k) {
   static const int mode = [] {
     const char* s = std::getenv("TMB_EIG_2STAGE");
     return s ? std::atoi(s) : -1;
   }();
   if (n < 4 * SBR_B || mode == 0) return false;
+  // size limits: stage 2 keeps the band in one 16-CTA cluster (n <= 8000), and the band
+  // inverse iteration stores each vector's banded LU (97 doubles per row) -- beyond
+  // ~16 GB of it (k = n = 8000 would be 50 GB) the one-stage path is used
+  if (n > 8000 || (double)k * (double)n * 97.0 * 8.0 > 16e9) return false;
   // measured crossover (scripts/gpu_s3_ab.sh, two-stage vs one-stage with the
   // shared-memory hand-off): n = 7680 239 vs 402 ms (k = 960), n = 5000 114 vs
   // 131 ms (k = 600), n = 4320 92 vs 88 ms (k = 540), n = 3840 82 vs 64 ms (k = 960)
@@ -1982,7 +1986,7 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
     LAUNCHED("k_jacobi");
     return;
   }
-  if (two_stage_for(n) && eig_two_stage(c, g, n, k, vecs, vals)) return;
+  if (two_stage_for(n, k) && eig_two_stage(c, g, n, k, vecs, vals)) return;
   const size_t mk = c.arena.mark();
   double* A = alloc<double>(c, (size_t)n * n);
   // Householder vectors: columns 0..n-3 written by k_sytrd, the rest (up to a

@@ -1119,6 +1119,41 @@ __global__ void k_larft(const double* __restrict__ S, const double* __restrict__
   for (int e = r; e < nb * nb; e += blockDim.x) T[(int64_t)p * nb * nb + e] = sT[e];
 }
 
+// The same T factor with thread r owning row r of T in registers: T(r, i) for
+// i > r only needs row r's own earlier entries and column i of S, so the rows
+// proceed independently -- no block barrier per column (the barrier-per-column
+// k_larft above spent ~76 us per 64-reflector panel on its serial chain).
+template <int NB>
+__global__ void __launch_bounds__(NB) k_larft_rows(const double* __restrict__ S, const double* __restrict__ tau,
+                                                   double* __restrict__ T) {
+  __shared__ double sS[NB * NB], st[NB];
+  const int p = blockIdx.x, r = threadIdx.x;
+  const double* Sp = S + (int64_t)p * NB * NB;
+  for (int e = r; e < NB * NB; e += NB) sS[e] = Sp[e];
+  st[r] = tau[(int64_t)p * NB + r];
+  __syncthreads();
+  double tr[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    double v = 0.0;
+    if (i == r) {
+      v = st[i];
+    } else if (i > r) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int cc = 0; cc < i; cc += 2) {
+        if (cc >= r) s0 = fma(tr[cc], sS[cc + NB * i], s0);
+        if (cc + 1 < i && cc + 1 >= r) s1 = fma(tr[cc + 1], sS[cc + 1 + NB * i], s1);
+      }
+      v = -st[i] * (s0 + s1);
+    }
+    tr[i] = v;
+  }
+  double* Tp = T + (int64_t)p * NB * NB;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) Tp[r + NB * i] = tr[i];
+}
+
 // ------------------------------------------------------------------ cluster repair
 // Robust path for (near-)repeated eigenvalues (a rank-deficient Gram asked for
 // more vectors than its rank, e.g. hosvd of a (100, 3, 3) tensor: 91 zero
@@ -1754,8 +1789,12 @@ static void backtransform(Ctx& c, const double* hv, const double* tau, int64_t n
     g.C = S; g.sCm = 1; g.sCn = nb; g.sCb = nb * nb;
     gemm(c, g);
   }
-  set_smem_attr(c, (const void*)k_larft, sizeof(double) * (2 * 64 * 64 + 64));
-  k_larft<<<np, nb, sizeof(double) * (2 * nb * nb + nb), c.stream>>>(S, tau, nb, T);
+  if (nb == 64) {
+    k_larft_rows<64><<<np, 64, 0, c.stream>>>(S, tau, T);
+  } else {
+    set_smem_attr(c, (const void*)k_larft, sizeof(double) * (2 * 64 * 64 + 64));
+    k_larft<<<np, nb, sizeof(double) * (2 * nb * nb + nb), c.stream>>>(S, tau, nb, T);
+  }
   LAUNCHED("k_larft");
   // (A fused one-kernel variant that streams every panel through shared memory
   // measured 3.0 ms vs ~1 ms for these GEMMs at n=1920: it is smem-bandwidth

@@ -30,6 +30,7 @@ int guard(tmb_ctx* ctx, F&& f) {
   auto rewind = [&]() {
     cudaStreamSynchronize(ctx->c.stream);
     cudaGetLastError();
+    ctx->c.oz_clear();  // cache slots point into the released arena frame
     ctx->c.arena.release(mk);
   };
   try {

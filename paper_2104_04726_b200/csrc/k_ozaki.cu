@@ -688,6 +688,16 @@ CUtensorMap digit_map(int8_t* base, int64_t rows, int64_t Kp, uint32_t box_rows,
 
 }  // namespace
 
+void ozaki_cache_slot(Ctx& c, int i, const void* x, DType tx, int64_t L, int64_t K, int64_t R) {
+  const int64_t MX = L * R;
+  const int64_t Xp = ceil_div(MX, OZ_BN) * OZ_BN, Kp = ceil_div(K, OZ_BK) * OZ_BK;
+  Ctx::OzSlot& z = c.ozs[i];
+  z = Ctx::OzSlot{};
+  z.ex = alloc<int>(c, (size_t)Xp);
+  z.sx = alloc<int8_t>(c, (size_t)OZ_S * Xp * Kp);
+  z.x = x; z.L = L; z.K = K; z.R = R; z.tx = (int)tx;
+}
+
 bool ozaki_enabled() {
   static const bool on = [] {
     const char* s = std::getenv("TMB_OZAKI");  // 0 = DMMA for every contraction
@@ -710,13 +720,18 @@ void ozaki_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t R,
   const int64_t Xp = ceil_div(MX, bn) * bn, Up = ceil_div(N, OZ_BM) * OZ_BM, Kp = ceil_div(K, OZ_BK) * OZ_BK;
   if (K > 65536) throw Error(TMB_EINVAL, "ozaki_ttm: K too large for int32 digit accumulation");
   const size_t mk = c.arena.mark();
-  int* ex = alloc<int>(c, (size_t)Xp);
+  Ctx::OzSlot* slot = nullptr;  // the operand's digit planes from an earlier pass of this solve
+  for (auto& z : c.ozs)
+    if (z.x == x && z.L == L && z.K == K && z.R == R && z.tx == (int)tx && n64) slot = &z;
+  int* ex = slot ? slot->ex : alloc<int>(c, (size_t)Xp);
   int* eu = alloc<int>(c, (size_t)Up);
-  int8_t* sx = alloc<int8_t>(c, (size_t)OZ_S * Xp * Kp);
+  int8_t* sx = slot ? slot->sx : alloc<int8_t>(c, (size_t)OZ_S * Xp * Kp);
   int8_t* su = alloc<int8_t>(c, (size_t)OZ_S * Up * Kp);
   // algorithmic work of the fp64-equivalent product: 2 MX N K
   Timed timed(c, TAG_OZAKI, 2.0 * (double)MX * N * K);  // fp64-equivalent flops
-  if (tx == F32 && L % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0) {
+  if (slot && slot->valid) {
+    // digit planes and row exponents already in place
+  } else if (tx == F32 && L % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0) {
     k_oz_rowexp_v4<<<(unsigned)ceil_div(MX, 128), 256, 0, c.stream>>>((const float*)x, L, K, R, ex);
   } else if (L >= 32) {
     if (tx == F32) k_oz_rowexp<float><<<(unsigned)ceil_div(MX, 32), 256, 0, c.stream>>>((const float*)x, L, K, R, ex);
@@ -727,13 +742,16 @@ void ozaki_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t R,
     else
       k_oz_rowexp<double><<<(unsigned)ceil_div(MX * 32, 256), 256, 0, c.stream>>>((const double*)x, L, K, R, ex);
   }
-  c.launches++;
-  check_launch("k_oz_rowexp");
-  dim3 ga((unsigned)ceil_div(Kp, 128), (unsigned)ceil_div(Xp, 32));
-  if (tx == F32) k_oz_sliceA<float><<<ga, 256, 0, c.stream>>>((const float*)x, L, K, R, ex, Xp, Kp, sx);
-  else k_oz_sliceA<double><<<ga, 256, 0, c.stream>>>((const double*)x, L, K, R, ex, Xp, Kp, sx);
-  c.launches++;
-  check_launch("k_oz_sliceA");
+  if (!(slot && slot->valid)) {
+    c.launches++;
+    check_launch("k_oz_rowexp");
+    dim3 ga((unsigned)ceil_div(Kp, 128), (unsigned)ceil_div(Xp, 32));
+    if (tx == F32) k_oz_sliceA<float><<<ga, 256, 0, c.stream>>>((const float*)x, L, K, R, ex, Xp, Kp, sx);
+    else k_oz_sliceA<double><<<ga, 256, 0, c.stream>>>((const double*)x, L, K, R, ex, Xp, Kp, sx);
+    c.launches++;
+    check_launch("k_oz_sliceA");
+    if (slot) slot->valid = true;
+  }
   k_oz_colexp<<<(unsigned)ceil_div(N * 32, 256), 256, 0, c.stream>>>(mat, K, N, sMr, sMk, eu);
   c.launches++;
   check_launch("k_oz_colexp");

@@ -132,6 +132,18 @@ int64_t prod(const Dims& d, int a, int b) {
   return p;
 }
 
+// whether ttm_dev sends the (L, K, Rr) -> r contraction to the Ozaki kernel (see ttm_dev)
+static bool ozaki_for(int64_t L, int64_t K, int64_t Rr, int64_t r) {
+  static const int oz_mode0 = [] {
+    const char* e = std::getenv("TMB_OZ_MODE0");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  if (K <= 64 && r <= 64) return false;  // small_ttm
+  const double flops = 2.0 * (double)L * Rr * K * r;
+  const bool mode0_oz = L == 1 && (oz_mode0 == 1 || (oz_mode0 < 0 && flops >= 1e11));
+  return ozaki_enabled() && (L >= 32 || mode0_oz) && flops >= 8e9 && K < 65536 && L * Rr <= 32LL * 65535 - 128;
+}
+
 void ttm_dev(Ctx& c, const void* x, DType tx, const Dims& dims, int mode, const double* m, int64_t r,
              int64_t sMr, int64_t sMk, double* y) {
   const int N = (int)dims.size();
@@ -148,13 +160,7 @@ void ttm_dev(Ctx& c, const void* x, DType tx, const Dims& dims, int mode, const 
   // TMB_OZ_MODE0=0 / 1: never / always for mode 0.
   // (launch-grid limit: the digit split and GEMM grids have L*Rr/32 and L*Rr/64 rows in
   // gridDim.y <= 65535; K < 65536 keeps 8*64*64*K digit products inside int32)
-  static const int oz_mode0 = [] {
-    const char* e = std::getenv("TMB_OZ_MODE0");
-    return e ? (e[0] == '1' ? 1 : 0) : -1;
-  }();
-  const double flops = 2.0 * (double)L * Rr * K * r;
-  const bool mode0_oz = L == 1 && (oz_mode0 == 1 || (oz_mode0 < 0 && flops >= 1e11));
-  if (ozaki_enabled() && (L >= 32 || mode0_oz) && flops >= 8e9 && K < 65536 && L * Rr <= 32LL * 65535 - 128) {
+  if (ozaki_for(L, K, Rr, r)) {
     ozaki_ttm(c, x, tx, L, K, Rr, m, r, sMr, sMk, y);
     return;
   }
@@ -529,6 +535,17 @@ void tucker_als_dev(Ctx& c, const void* x, DType tx, const Dims& dims, const Dim
   const double tn = std::sqrt(tsq);
   if (tn == 0.0) throw Error(TMB_EINVAL, "cannot decompose the zero tensor");  // tucker.py:341-342
   const size_t mk = c.arena.mark();
+  // the two full passes over the raw tensor every sweep (mode 1, then mode 0 after the
+  // mode-0 update) re-split the same operand: keep its Ozaki digit planes for the solve
+  // (C2: the 498 MB mode-1 planes; C5: 14.3 GB per pass). Also used by the T-HOSVD core.
+  c.oz_clear();
+  if (N >= 2) {
+    int slot = 0;
+    if (ozaki_for(dims[0], dims[1], prod(dims, 2, N), ranks[1]))
+      ozaki_cache_slot(c, slot++, x, tx, dims[0], dims[1], prod(dims, 2, N));
+    if (ozaki_for(1, dims[0], prod(dims, 1, N), ranks[0]))
+      ozaki_cache_slot(c, slot++, x, tx, 1, dims[0], prod(dims, 1, N));
+  }
   // model buffers: current (a), candidate (b), best
   auto model_alloc = [&](std::vector<double*>& f) -> double* {
     f.resize(N);
@@ -632,6 +649,7 @@ void tucker_als_dev(Ctx& c, const void* x, DType tx, const Dims& dims, const Dim
   for (int n = 0; n < N; ++n) copy_d(c, factors_out[n], (*out_f)[n], dims[n] * ranks[n]);
   if (trace) { trace->converged = converged ? 1 : 0; trace->best_index = out_idx; }
   TMB_CUDA(cudaStreamSynchronize(c.stream));
+  c.oz_clear();
   c.arena.release(mk);
 }
 

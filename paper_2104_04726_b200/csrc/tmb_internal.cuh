@@ -76,6 +76,19 @@ struct Ctx {
   KernelTimes kt;
   double work[TAG_COUNT] = {0};    // algorithmic flops/bytes attributed per tag
   int gemm_tag = TAG_GEMM;         // TAG_EIG_GEMM while inside the eigen-solver
+  // Ozaki digit planes of a tensor operand kept for the rest of one solve (tucker_als
+  // re-splits the same raw tensor identically every sweep otherwise): buffers from the
+  // solve's arena frame, registered by ozaki_cache_begin, filled on first use.
+  struct OzSlot {
+    const void* x = nullptr;
+    int64_t L = 0, K = 0, R = 0;
+    int tx = -1;
+    int8_t* sx = nullptr;
+    int* ex = nullptr;
+    bool valid = false;
+  };
+  OzSlot ozs[2];
+  void oz_clear() { for (auto& z : ozs) z = OzSlot{}; }
 };
 
 // RAII: records an event pair around the launches in its scope (if enabled)
@@ -202,6 +215,10 @@ void decode_sse(Ctx& c, const double* t, int64_t n_img, int64_t h, int64_t w, in
 // y = x x_n mat over the GEMM view rows (i < L, l < R), K = dims[n], N = rows of mat
 // (mat(r, k) at mat[r sMr + k sMk]); fp64-equivalent via int8 digit products.
 bool ozaki_enabled();
+// register (and allocate from the current arena frame) a digit-plane cache slot for the
+// tensor operand x viewed as (L, K, R) with K contracted; ozaki_ttm reuses it when asked
+// for the same operand again before c.oz_clear()
+void ozaki_cache_slot(Ctx& c, int slot, const void* x, DType tx, int64_t L, int64_t K, int64_t R);
 void ozaki_ttm(Ctx& c, const void* x, DType tx, int64_t L, int64_t K, int64_t R, const double* mat, int64_t N,
                int64_t sMr, int64_t sMk, double* y);
 

@@ -140,7 +140,7 @@ static bool ozaki_for(int64_t L, int64_t K, int64_t Rr, int64_t r) {
   }();
   if (K <= 64 && r <= 64) return false;  // small_ttm
   const double flops = 2.0 * (double)L * Rr * K * r;
-  const bool mode0_oz = L == 1 && (oz_mode0 == 1 || (oz_mode0 < 0 && flops >= 1e11));
+  const bool mode0_oz = L == 1 && (oz_mode0 == 1 || (oz_mode0 < 0 && flops >= 2e10));
   return ozaki_enabled() && (L >= 32 || mode0_oz) && flops >= 8e9 && K < 65536 && L * Rr <= 32LL * 65535 - 128;
 }
 
@@ -154,10 +154,10 @@ void ttm_dev(Ctx& c, const void* x, DType tx, const Dims& dims, int mode, const 
   }
   // full passes over the tensor (>= 8 GFLOP) with the contracted mode not the first:
   // Ozaki int8 digit products on tcgen05 (measured at C2: mode 1 1.62 vs 1.96 ms on
-  // DMMA). The mode-0 pass only from 100 GFLOP: at C2 (34 GFLOP) the two engines tie
-  // (ozaki + gemm families 95 ms per stack either way), at C5 (1.9 TFLOP) Ozaki saves
-  // 0.24 s per stack (gemm 1786 -> 1090 ms, ozaki 693 -> 1150 ms; scripts/gpu_s3_oz0.sh).
-  // TMB_OZ_MODE0=0 / 1: never / always for mode 0.
+  // DMMA). The mode-0 pass from 20 GFLOP: with the digit planes of the raw tensor kept
+  // across the sweeps (ozaki_cache_slot) it saves 9 ms per C2 stack (34 GFLOP passes;
+  // 424 -> 415 ms) and 0.24 s per C5 stack (1.9 TFLOP; gemm 1786 -> 1090 ms); C3's
+  // 17 GFLOP passes tie. TMB_OZ_MODE0=0 / 1: never / always for mode 0.
   // (launch-grid limit: the digit split and GEMM grids have L*Rr/32 and L*Rr/64 rows in
   // gridDim.y <= 65535; K < 65536 keeps 8*64*64*K digit products inside int32)
   if (ozaki_for(L, K, Rr, r)) {

@@ -1,7 +1,6 @@
 // Two-stage tridiagonalisation for eigh (tensor.py:195) of the large Grams
-// (C4 / C5: n = 2160 ... 7680), where the one-stage reduction is bound by a
-// grid barrier per column (n <= 2048, Gram in shared memory) or by streaming
-// the trailing matrix from HBM once per column (larger n).
+// (the default for n > 4600: C5's n = 7680), where the one-stage reduction
+// streams the trailing matrix from HBM / L2 once per column.
 //
 //  stage 1 (sy2sb): dense -> band of half-bandwidth SBR_B. Panel p (columns
 //    p0 .. p0+31) is QR-factorised below the band by ONE thread-block cluster
@@ -615,7 +614,7 @@ constexpr int IV_W = 4;                 // warps (eigenvalues) per block
 constexpr int IV_R = SB + 1;            // window rows
 constexpr int IV_C = 2 * SB + 1;        // window columns = U row length
 constexpr int IV_WIN = (IV_R * IV_C + 1) / 2 * 2;  // window, rounded to 16 bytes
-constexpr int IV_SMEM_WARP = (IV_WIN + 32 + IV_R + IV_C + 1) / 2 * 2;  // per-warp base stays 16-byte aligned
+constexpr int IV_SMEM_WARP = (IV_WIN + IV_R + IV_C + 1) / 2 * 2;  // per-warp base stays 16-byte aligned
 
 __device__ __forceinline__ double start_entry(int64_t vi, int64_t i) {
   uint64_t h = (uint64_t)vi * 0x9E3779B97F4A7C15ull ^ ((uint64_t)i + 0x632BE59BD9B4E019ull);
@@ -653,8 +652,7 @@ __global__ void __launch_bounds__(IV_W * 32) k_band_invit(const double* __restri
   const int64_t vi = (int64_t)blockIdx.x * IV_W + warp;
   if (vi >= k) return;
   double* W = smi + (size_t)warp * IV_SMEM_WARP;  // [row % IV_R][col % IV_C]
-  double* mult = W + IV_WIN;
-  double* yw = mult + 32;                         // forward window (IV_R)
+  double* yw = W + IV_WIN;                        // forward window (IV_R)
   double* xw = yw + IV_R;                         // back window (IV_C)
   const double sigma = vals[vi];
   const double tiny = DBL_EPSILON * fmax(*bnorm, DBL_MIN);

@@ -435,46 +435,68 @@ __device__ __forceinline__ void s2_task_fast(double* base, double* base2, int h,
   }
 }
 
-template <int CS, bool PROF>
+// Rows are split into NG = CS * RPC ranges of R rows. RPC = 1 (default): CTA c owns
+// range c. RPC = 2 (TMB_S2_MIRROR=1, 16-CTA cluster): CTA c owns ranges c and
+// 2CS-1-c, a top and the mirrored bottom one, each served by half of its warps --
+// row r is touched by ~r/b tasks, so contiguous ranges give the last CTA twice the
+// average task count; the mirrored pairs balance it but measured slower (sb2st()).
+template <int CS, int RPC, bool PROF>
 __global__ void __launch_bounds__(S2_W * 32, 1) k_sb2st(const S2Args a) {
+  constexpr int NG = CS * RPC;       // ranges
+  constexpr int WP = S2_W / RPC;     // warps per range (slot)
   extern __shared__ __align__(16) double sm[];
   cg::cluster_group cl = cg::this_cluster();
   const int cr = CS > 1 ? (int)cl.block_rank() : 0;
-  const int n = a.n, R = a.R, RS = a.RS;
-  double* rows = sm;                                    // RS x S2_LDL
-  double* hbox = rows + (size_t)RS * S2_LDL;            // S2_NS x 33 (v, tau) mailboxes
-  double* scr = hbox + S2_NS * 33;                      // per warp: vs, ws, zs (3 x 32)
-  unsigned* lprog = reinterpret_cast<unsigned*>(scr + S2_W * 96);
+  const int n = a.n, R = a.R, RS = a.RS;  // R: rows per range; RS: rows of this CTA in shared memory
+  double* rows = sm;                                    // RS x S2_LDL (slot 0's rows, then slot 1's)
+  double* hbox = rows + (size_t)RS * S2_LDL;            // RPC x S2_NS x 33 (v, tau) mailboxes
+  double* scr = hbox + RPC * S2_NS * 33;                // per warp: vs, ws, zs (3 x 32)
+  unsigned* lprog = reinterpret_cast<unsigned*>(scr + S2_W * 96);  // RPC x S2_NS
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int lo = cr * R, hi = min(n, lo + R);
-  auto rowp_of = [&](int r, int owner, double* base) -> double* {
-    const int lr = r - owner * R;
-    if (lr < RS) return base + (size_t)lr * S2_LDL;
-    return a.spill + ((size_t)owner * (R - RS) + (lr - RS)) * S2_LDL;
+  const int SPILL = RPC * R - RS;                       // spill rows per CTA
+  auto owner = [](int g) { return RPC == 1 || g < CS ? g : 2 * CS - 1 - g; };
+  auto slot = [](int g) { return RPC == 1 || g < CS ? 0 : 1; };
+  // row r of range g (owned by CTA owner(g), slot slot(g)) given that CTA's rows base
+  auto rowp_g = [&](int r, int g, double* base) -> double* {
+    const int li = slot(g) * R + (r - g * R);
+    if (li < RS) return base + (size_t)li * S2_LDL;
+    return a.spill + ((size_t)owner(g) * SPILL + (li - RS)) * S2_LDL;
   };
-  for (int e = tid; e < (hi - lo) * S2_LDL; e += S2_W * 32) {
-    const int r = lo + e / S2_LDL, o = e % S2_LDL;
-    double v = 0.0;
-    if (o <= SB && r - o >= 0) v = a.band[(size_t)r * (2 * SB + 1) + (SB - o)];
-    rowp_of(r, cr, rows)[o] = v;
+  for (int sl = 0; sl < RPC; ++sl) {
+    const int g = sl == 0 ? cr : 2 * CS - 1 - cr;
+    const int glo = g * R, ghi = min(n, glo + R);
+    for (int e = tid; e < max(0, ghi - glo) * S2_LDL; e += S2_W * 32) {
+      const int r = glo + e / S2_LDL, o = e % S2_LDL;
+      double v = 0.0;
+      if (o <= SB && r - o >= 0) v = a.band[(size_t)r * (2 * SB + 1) + (SB - o)];
+      rowp_g(r, g, rows)[o] = v;
+    }
   }
-  for (int e = tid; e < S2_NS; e += S2_W * 32) lprog[e] = 0u;
+  for (int e = tid; e < RPC * S2_NS; e += S2_W * 32) lprog[e] = 0u;
   if constexpr (CS > 1) cl.sync(); else __syncthreads();
+  // this warp's range and its neighbours
+  const int sl = warp / WP, wl = warp % WP;
+  const int g = sl == 0 ? cr : 2 * CS - 1 - cr;
+  const int lo = g * R, hi = min(n, lo + R);
+  auto cta_ptr = [&](auto* p, int c) {
+    if constexpr (CS > 1) return c == cr ? p : cl.map_shared_rank(p, c);
+    else return p;
+  };
   double* rows_nx = rows;
-  double* hbox_nx = hbox;
+  double* hbox_nx = nullptr;
   unsigned* lp_nx = nullptr;
   unsigned* lp_pv = nullptr;
-  if constexpr (CS > 1) {
-    if (cr + 1 < CS) {
-      rows_nx = cl.map_shared_rank(rows, cr + 1);
-      hbox_nx = cl.map_shared_rank(hbox, cr + 1);
-      lp_nx = cl.map_shared_rank(lprog, cr + 1);
-    }
-    if (cr > 0) lp_pv = cl.map_shared_rank(lprog, cr - 1);
+  if (g + 1 < NG) {
+    rows_nx = cta_ptr(rows, owner(g + 1));
+    hbox_nx = cta_ptr(hbox, owner(g + 1)) + slot(g + 1) * S2_NS * 33;
+    lp_nx = cta_ptr(lprog, owner(g + 1)) + slot(g + 1) * S2_NS;
   }
+  if (g > 0) lp_pv = cta_ptr(lprog, owner(g - 1)) + slot(g - 1) * S2_NS;
+  double* my_hbox = hbox + sl * S2_NS * 33;
+  unsigned* my_lp = lprog + sl * S2_NS;
   auto wait_for = [&](int s, int cnt, bool remote) {
     const unsigned want = tag(s, cnt);
-    const unsigned* p = lprog + (s % S2_NS);
+    const unsigned* p = my_lp + (s % S2_NS);
     if (remote) {
       while (ld_acq_cl(p) < want) __nanosleep(64);
     } else {
@@ -486,17 +508,20 @@ __global__ void __launch_bounds__(S2_W * 32, 1) k_sb2st(const S2Args a) {
   double* zs = vs + 64;
   long long pw = 0, pt = 0, pn = 0;
   long long ph[5] = {0, 0, 0, 0, 0};
-  for (int s = warp; s <= n - 3; s += S2_W) {
+  // the first run of a task's rows: this range's shared rows, then its spill rows
+  const int li0 = slot(g) * R;                                  // local index of row lo
+  const int lsm = li0 >= RS ? lo : lo + min(RS - li0, hi - lo);  // end of the range's shared rows
+  for (int s = wl; s <= n - 3; s += WP) {
     if (s + 1 >= hi) break;
     const int jst = lo > s + 1 ? (lo - s - 1 + SB - 1) / SB : 0;
     if (s + 1 + jst * SB >= hi) continue;
     double vp = 0.0, taup = 0.0;
-    if (jst > 0) {  // reflector of (s, jst - 1) from the previous CTA
+    if (jst > 0) {  // reflector of (s, jst - 1) from the previous range
       const long long t0 = PROF ? clock64() : 0;
       wait_for(s, jst, true);
       if constexpr (PROF) pw += clock64() - t0;
-      vp = hbox[(s % S2_NS) * 33 + lane];
-      taup = hbox[(s % S2_NS) * 33 + 32];
+      vp = my_hbox[(s % S2_NS) * 33 + lane];
+      taup = my_hbox[(s % S2_NS) * 33 + 32];
     }
     const int jlast_prev = (n - 1 - s) / SB;  // last position of sweep s-1: s + j SB < n
     for (int j = jst;; ++j) {
@@ -504,7 +529,7 @@ __global__ void __launch_bounds__(S2_W * 32, 1) k_sb2st(const S2Args a) {
       if (q0 >= hi) break;
       const long long t0 = PROF ? clock64() : 0;
       if (s > 0) {
-        // (s-1, jd) ran on this CTA (CTA scope) or on the next one (cluster scope)
+        // (s-1, jd) ran in this range (CTA scope) or in the next one (cluster scope)
         const int jd = min(j + 1, jlast_prev);
         wait_for(s - 1, jd + 1, s + jd * SB >= hi);
       }
@@ -512,22 +537,19 @@ __global__ void __launch_bounds__(S2_W * 32, 1) k_sb2st(const S2Args a) {
       pw += t1 - t0;
       const int m = min(SB, n - q0);
       double v, tau;
-      // rows q0 .. q0+m-1 as one or two runs of consecutive rows: this CTA's
-      // shared rows [lo, lo+RS), its spill rows [lo+RS, hi), the next CTA's rows
-      const int lsm = lo + min(RS, hi - lo);  // end of this CTA's shared-memory rows
-      double* b1 = q0 < lsm ? rows + (size_t)(q0 - lo) * S2_LDL
-                            : a.spill + ((size_t)cr * (R - RS) + (q0 - lsm)) * S2_LDL;
+      double* b1 = q0 < lsm ? rowp_g(q0, g, rows) : rowp_g(q0, g, rows);
       const int e1 = q0 < lsm ? lsm : hi;  // end of the first run
       long long* php = ph;
       if (q0 + m <= e1) {
         if (m == SB) s2_task_fast<false, false, PROF>(b1, b1, m, m, j, lane, vp, taup, vs, ws, zs, v, tau, php);
         else s2_task_fast<false, true, PROF>(b1, b1, m, m, j, lane, vp, taup, vs, ws, zs, v, tau, php);
       } else {
-        double* b2 = e1 == lsm && lsm < hi ? a.spill + (size_t)cr * (R - RS) * S2_LDL : rows_nx;
+        // second run: this range's spill rows, or the next range's first rows (shared memory)
+        double* b2 = e1 < hi ? rowp_g(e1, g, rows) : rowp_g(hi, g + 1, rows_nx);
         if (m == SB) s2_task_fast<true, false, PROF>(b1, b2, e1 - q0, m, j, lane, vp, taup, vs, ws, zs, v, tau, php);
         else s2_task_fast<true, true, PROF>(b1, b2, e1 - q0, m, j, lane, vp, taup, vs, ws, zs, v, tau, php);
       }
-      // hand-off to the next CTA, then publish progress (release at cluster scope)
+      // hand-off to the next range, then publish progress
       const int q0n = q0 + SB;
       if (q0n < n && q0n >= hi) {
         hbox_nx[(s % S2_NS) * 33 + lane] = v;
@@ -535,10 +557,10 @@ __global__ void __launch_bounds__(S2_W * 32, 1) k_sb2st(const S2Args a) {
       }
       __syncwarp();
       if (lane == 0) {
-        // local consumers: (s, j+1) here and (s+1, j-1) here; the previous CTA
-        // waits only on this sweep's first task here, the next CTA on the last
+        // local consumers: (s, j+1) and (s+1, j-1) in this range; the previous range
+        // waits only on this sweep's first task here, the next range on the last
         const unsigned t = tag(s, j + 1);
-        red_max_rel_cta(lprog + (s % S2_NS), t);
+        red_max_rel_cta(my_lp + (s % S2_NS), t);
         if (lp_nx && q0n < n && q0n >= hi) red_max_rel_cl(lp_nx + (s % S2_NS), t);
         if (lp_pv && j == jst) red_max_rel_cl(lp_pv + (s % S2_NS), t);
       }
@@ -554,10 +576,14 @@ __global__ void __launch_bounds__(S2_W * 32, 1) k_sb2st(const S2Args a) {
     for (int t = 0; t < 5; ++t) q[3 + t] = ph[t];
   }
   if constexpr (CS > 1) cl.sync(); else __syncthreads();
-  for (int r = lo + tid; r < hi; r += S2_W * 32) {
-    const double* rr = rowp_of(r, cr, rows);
-    a.d[r] = rr[0];
-    if (r >= 1) a.e[r - 1] = rr[1];
+  for (int s2 = 0; s2 < RPC; ++s2) {
+    const int g2 = s2 == 0 ? cr : 2 * CS - 1 - cr;
+    const int glo = g2 * R, ghi = min(n, glo + R);
+    for (int r = glo + tid; r < ghi; r += S2_W * 32) {
+      const double* rr = rowp_g(r, g2, rows);
+      a.d[r] = rr[0];
+      if (r >= 1) a.e[r - 1] = rr[1];
+    }
   }
   if constexpr (CS > 1) cl.sync();
 }
@@ -983,20 +1009,25 @@ void band_rows(Ctx& c, const double* A, int64_t n, double* band) {
 }
 
 namespace {
-constexpr size_t S2_FIXED = sizeof(double) * (S2_NS * 33 + S2_W * 96) + sizeof(unsigned) * S2_NS;
-constexpr int S2_MAXRS = (int)((227 * 1024 - S2_FIXED) / (sizeof(double) * S2_LDL));
+template <int RPC>
+constexpr size_t s2_fixed() {
+  return sizeof(double) * (RPC * S2_NS * 33 + S2_W * 96) + sizeof(unsigned) * RPC * S2_NS;
+}
+constexpr int S2_MAXRS = (int)((227 * 1024 - s2_fixed<2>()) / (sizeof(double) * S2_LDL));
 
-template <int CS>
+template <int CS, int RPC>
 void sb2st_cs(Ctx& c, const double* band, int n, double* d, double* e) {
-  const int R = (n + CS - 1) / CS;
-  // rows kept in shared memory; a spill region, when needed, holds >= SB rows so
-  // a task's 32 rows never span more than two runs (smem | spill | next CTA)
-  const int RS = R <= S2_MAXRS ? R : std::min(S2_MAXRS, R - SB);
-  const size_t smem = S2_FIXED + sizeof(double) * (size_t)RS * S2_LDL;
+  const int R = (n + CS * RPC - 1) / (CS * RPC);  // rows per range
+  // rows kept in shared memory per CTA (its RPC ranges back to back); a spill region,
+  // when needed, holds >= SB rows so a task's 32 rows never span more than two runs,
+  // and every range's first SB rows stay in shared memory
+  const int RS = RPC * R <= S2_MAXRS ? RPC * R : std::min(S2_MAXRS, RPC * R - SB);
+  if (RPC == 2 && RS < R + SB) throw Error(TMB_EINVAL, "sb2st: band rows do not fit the cluster");
+  const size_t smem = s2_fixed<RPC>() + sizeof(double) * (size_t)RS * S2_LDL;
   const size_t mk = c.arena.mark();
-  double* spill = R > RS ? alloc<double>(c, (size_t)CS * (R - RS) * S2_LDL) : nullptr;
+  double* spill = RPC * R > RS ? alloc<double>(c, (size_t)CS * (RPC * R - RS) * S2_LDL) : nullptr;
   static const bool prof_on = std::getenv("TMB_S2_PROF") != nullptr;
-  const void* kfn = prof_on ? (const void*)k_sb2st<CS, true> : (const void*)k_sb2st<CS, false>;
+  const void* kfn = prof_on ? (const void*)k_sb2st<CS, RPC, true> : (const void*)k_sb2st<CS, RPC, false>;
   set_smem_attr(c, kfn, smem);
   if (CS > 8) allow_cluster16(c, kfn);
   long long* prof = nullptr;
@@ -1006,8 +1037,8 @@ void sb2st_cs(Ctx& c, const double* band, int n, double* d, double* e) {
   }
   S2Args a{band, n, R, RS, spill, d, e, prof};
   void* args[] = {&a};
-  if (prof_on) launch_cluster(c, k_sb2st<CS, true>, CS, dim3(CS), S2_W * 32, smem, args);
-  else launch_cluster(c, k_sb2st<CS, false>, CS, dim3(CS), S2_W * 32, smem, args);
+  if (prof_on) launch_cluster(c, k_sb2st<CS, RPC, true>, CS, dim3(CS), S2_W * 32, smem, args);
+  else launch_cluster(c, k_sb2st<CS, RPC, false>, CS, dim3(CS), S2_W * 32, smem, args);
   LAUNCHED("k_sb2st");
   if (prof) {
     std::vector<long long> h((size_t)CS * S2_W * 8);
@@ -1031,14 +1062,22 @@ void sb2st_cs(Ctx& c, const double* band, int n, double* d, double* e) {
 }  // namespace
 
 void sb2st(Ctx& c, const double* band, int64_t n, double* d, double* e) {
-  // rows per CTA R: >= SB (a task spans at most two CTAs) and < 63 S2_W (the
-  // warps of one CTA can never wait on a later sweep they own themselves)
+  // rows per range R: >= SB (a task spans at most two ranges) and < 63 x (warps per
+  // range) (the warps of one range can never wait on a later sweep they own
+  // themselves). TMB_S2_MIRROR=1 pairs mirrored ranges on the 16-CTA cluster (balances
+  // the per-CTA task counts; measured slower: n = 7680 244 vs 239 ms, n = 4700 108 vs
+  // 105 ms -- half the warps per range, twice the range boundaries)
+  static const bool mirror = [] {
+    const char* s = std::getenv("TMB_S2_MIRROR");
+    return s && std::atoi(s) == 1;
+  }();
   const int N = (int)n;
-  if (n <= S2_MAXRS) sb2st_cs<1>(c, band, N, d, e);
-  else if (n <= 2 * S2_MAXRS) sb2st_cs<2>(c, band, N, d, e);
-  else if (n <= 4 * S2_MAXRS) sb2st_cs<4>(c, band, N, d, e);
-  else if (n <= 8 * S2_MAXRS) sb2st_cs<8>(c, band, N, d, e);
-  else if (ceil_div(n, 16) < 63 * S2_W) sb2st_cs<16>(c, band, N, d, e);
+  if (n <= S2_MAXRS) sb2st_cs<1, 1>(c, band, N, d, e);
+  else if (n <= 2 * S2_MAXRS) sb2st_cs<2, 1>(c, band, N, d, e);
+  else if (n <= 4 * S2_MAXRS) sb2st_cs<4, 1>(c, band, N, d, e);
+  else if (n <= 8 * S2_MAXRS) sb2st_cs<8, 1>(c, band, N, d, e);
+  else if (mirror && ceil_div(n, 32) < 63 * (S2_W / 2)) sb2st_cs<16, 2>(c, band, N, d, e);
+  else if (ceil_div(n, 16) < 63 * S2_W) sb2st_cs<16, 1>(c, band, N, d, e);
   else throw Error(TMB_EINVAL, "sb2st: band too large for one cluster");
 }
 

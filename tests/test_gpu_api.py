@@ -637,3 +637,30 @@ print("ok")
     env = dict(os.environ, TMB_EIG_2STAGE="1")
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-3000:]
+
+
+def test_ozaki_digit_cache_is_per_solve():
+    """The Ozaki digit planes of the raw tensor are kept only for one solve: two
+    different tensors solved one after the other IN THE SAME device buffer give
+    exactly what each gives in a buffer of its own (the cache is keyed by the
+    operand's address, so it must not survive the call). C2-size passes, so both
+    full passes go through the Ozaki kernel."""
+    import torch
+
+    from paper_2104_04726_b200.tucker import solve_device
+
+    dims = (1080, 1920, 3, 10)
+    cfg = tb.SolveConfig(ranks=(270, 480, 3, 5), max_sweeps=2, fit_tol=1e-300, pp_enter_tol=0.0)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    n = int(np.prod(dims))
+    xa = torch.rand(n, generator=g, device="cuda", dtype=torch.float32)
+    xb = torch.rand(n, generator=g, device="cuda", dtype=torch.float32) ** 2
+    shared = xa.clone()
+    solve_device(shared, L.F32, dims, cfg)          # fills the cache for `shared`'s address
+    shared.copy_(xb)
+    mb_shared, tb_shared = solve_device(shared, L.F32, dims, cfg)
+    mb_own, tb_own = solve_device(xb.clone(), L.F32, dims, cfg)
+    assert [r.fit for r in tb_shared.records] == [r.fit for r in tb_own.records]
+    assert np.array_equal(mb_shared.core.array, mb_own.core.array)
+    for u, v in zip(mb_shared.factors, mb_own.factors):
+        assert np.array_equal(u, v)

@@ -86,6 +86,9 @@ def parse(argv=None):
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(METRICS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--lanes", type=int, default=None,
+                    help="c3: concurrent solves per GPU (host threads with their own stream + context; "
+                         "default pipeline.DEFAULT_LANES)")
     return ap.parse_args(argv)
 
 
@@ -354,7 +357,8 @@ def run_ours(args) -> None:
     import paper_2104_04726_b200 as tb
     from paper_2104_04726_b200 import _lib as L
     from paper_2104_04726_b200.dist import assign_stacks
-    from paper_2104_04726_b200.pipeline import encode_stack_device
+    from paper_2104_04726_b200 import pipeline as P
+    from paper_2104_04726_b200.pipeline import encode_stack_device, encode_stacks_device, stream_lanes
 
     wl = args.workload
     cfg = CONFIGS[wl]
@@ -378,12 +382,21 @@ def run_ours(args) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    nl = 1 if wl == "c2" else max(1, min(P.DEFAULT_LANES if args.lanes is None else args.lanes, len(dev_stacks)))
+    ctxs = [h] + ([ln.ctx for ln in stream_lanes(nl)] if nl > 1 else [])
+
     def device_step(bufs):
+        if nl > 1:   # c3: stacks spread over concurrent lanes (pipeline.encode_stacks_device)
+            res = encode_stacks_device(dev_stacks, cfg.space, cfg.ranks, sc, cfg.qp, True, nl)
+            return bufs, (res[-1][0].records[-1].fit, res[-1][2])
         out = None
         for d in dev_stacks:
             bufs, tr, step, rel = encode_stack_device(d, cfg.space, cfg.ranks, sc, cfg.qp, True, bufs)
-            out = (tr, rel)
+            out = (float(tr.fit[tr.n_records - 1]), rel)
         return bufs, out
+
+    def launches_all() -> int:
+        return sum(int(L.LIB.tmb_launch_count(c)) for c in ctxs)
 
     # ---- device-resident throughput (value): inputs already in HBM
     bufs = None
@@ -392,8 +405,9 @@ def run_ours(args) -> None:
     clocks = ClockSampler(local)
     barrier()
     clocks.start()
-    L.check(L.LIB.tmb_timing(h, 1), h)
-    n0 = L.launch_count()
+    for c in ctxs:
+        L.check(L.LIB.tmb_timing(c, 1), c)
+    n0 = launches_all()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record()
@@ -401,19 +415,24 @@ def run_ours(args) -> None:
         bufs, last = device_step(bufs)
     ev1.record()
     barrier()
-    launches = L.launch_count() - n0
+    launches = launches_all() - n0
     clk = clocks.stop()
     my_ms = ev0.elapsed_time(ev1)
     ms = max_over_ranks(my_ms)
     fam = {}
     for tag, name in ((0, "gemm_dmma"), (1, "sytrd"), (2, "tridiag_vectors"), (3, "color_u8"),
                       (4, "eig_gemm_dmma"), (5, "ttm_ozaki_i8")):
-        cnt, tms, work = L.C.c_int64(), L.C.c_double(), L.C.c_double()
-        L.check(L.LIB.tmb_timing_read(h, tag, L.C.byref(cnt), L.C.byref(tms), L.C.byref(work)), h)
-        fam[name] = {"launches": cnt.value, "ms": tms.value, "work": work.value}
-    L.check(L.LIB.tmb_timing(h, 0), h)
+        fam[name] = {"launches": 0, "ms": 0.0, "work": 0.0}
+        for c in ctxs:
+            cnt, tms, work = L.C.c_int64(), L.C.c_double(), L.C.c_double()
+            L.check(L.LIB.tmb_timing_read(c, tag, L.C.byref(cnt), L.C.byref(tms), L.C.byref(work)), c)
+            fam[name]["launches"] += cnt.value
+            fam[name]["ms"] += tms.value
+            fam[name]["work"] += work.value
+    for c in ctxs:
+        L.check(L.LIB.tmb_timing(c, 0), c)
     value = units_total * args.steps / (ms / 1e3)
-    tr, rel = last
+    fit_last, rel = last
 
     # ---- HOOI sweep time: K-sweep solve minus 0-sweep solve (same stack)
     sc0 = tb.SolveConfig(ranks=cfg.ranks, max_sweeps=0, fit_tol=1e-300, pp_enter_tol=0.0)
@@ -434,7 +453,7 @@ def run_ours(args) -> None:
         if wl == "c2":
             r = tb.encode_stack(pinned[0], cfg.space, cfg.ranks, cfg.sweeps, cfg.qp)
             return [r]
-        return tb.encode_stacks(pinned, cfg.space, cfg.ranks, cfg.sweeps, cfg.qp)
+        return tb.encode_stacks(pinned, cfg.space, cfg.ranks, cfg.sweeps, cfg.qp, lanes=nl)
     for _ in range(args.warmup):      # also populates torch's pinned host-block cache used by the D2H
         res = e2e_step()
     barrier()
@@ -454,7 +473,7 @@ def run_ours(args) -> None:
             d2h += int(r.model.core.array.nbytes + sum(f.nbytes for f in r.model.factors))
     e2e = {"value": units_total * args.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "path": "encode_stack" if wl == "c2" else
-           "encode_stacks (H2D of stack i+1 on a copy stream overlapping the solve of stack i)"}
+           f"encode_stacks ({nl} lanes; per lane the H2D of its next stack on a copy stream overlaps its current solve)"}
 
     # ---- roofline of the dominant kernel family (live CUDA-event launch durations)
     dom_name, dom = max(fam.items(), key=lambda kv: kv[1]["ms"])
@@ -503,7 +522,7 @@ def run_ours(args) -> None:
     line = base_line(wl, world, args, value, ms / args.steps)
     line.update({
         "hooi_sweep_ms": sweep_ms,
-        "fit": float(tr.fit[tr.n_records - 1]), "rel_err": rel,
+        "fit": fit_last, "rel_err": rel,
         "e2e": e2e,
         "gpu_launches": int(launches),
         "roofline": roof,
@@ -513,6 +532,7 @@ def run_ours(args) -> None:
                             for k, v in fam.items()},
         "clocks": clk,
         "stacks_per_rank": len(ids),
+        "lanes": nl,
     })
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, host_stacks[0])

@@ -9,6 +9,7 @@
 // tensor is bit-identical to fp32(reference f64 colour). The IPT path uses a
 // host-built 256-entry EOTF table (the u8 codes are exact) and CUDA pow for
 // the 0.43 power; its matrix products follow the reference's 3x3 order.
+#include <mutex>
 #include <type_traits>
 
 #include "tmb_internal.cuh"
@@ -492,8 +493,10 @@ void inv3(const double* m, double* o) {
 }
 
 bool g_const_ready[64] = {false};
+std::mutex g_const_mu;  // contexts on several host threads (pipeline lanes) may arrive together
 
 void ensure_constants(Ctx& c) {
+  std::lock_guard<std::mutex> lk(g_const_mu);
   if (c.device >= 0 && c.device < 64 && g_const_ready[c.device]) return;
   ColorConst h{};
   for (int v = 0; v < 256; ++v) {

@@ -19,7 +19,7 @@ from . import _lib as L
 from .tensor import DenseTensor
 from .tucker import SolveConfig, SolveTrace, TuckerModel, _trace_buffers, _trace_from_c
 
-__all__ = ["StackResult", "encode_stack", "encode_stack_device", "encode_stacks", "coding_tensor", "ScenePSNR", "DecodedStack",
+__all__ = ["StackResult", "encode_stack", "encode_stack_device", "encode_stacks", "encode_stacks_device", "stream_lanes", "coding_tensor", "ScenePSNR", "DecodedStack",
            "decode_stack"]
 
 
@@ -112,38 +112,76 @@ def encode_stack(images_u8: np.ndarray, space: str, ranks: Sequence[int], sweeps
     return StackResult(model, _trace_from_c(tr), levels, step, rel, bufs)
 
 
-def encode_stacks(stacks, space: str, ranks: Sequence[int], sweeps: int, qp: int, fit_tol: float = 1e-300,
-                  pp_enter_tol: float = 0.0, rel_err: bool = True) -> list[StackResult]:
-    """Encode a sequence of independent stacks on this rank's GPU with the H2D
-    of stack i+1 overlapped with the device solve of stack i (BASELINE config 3,
-    SURVEY §8(e): "H2D of stack i+1's u8 planes overlaps compute of stack i").
+class _Lane:
+    """One host thread with its own CUDA stream and its own libtmb context
+    (``L.ctx()`` is per thread). Independent stacks on different lanes run
+    concurrently on the GPU: a stack's latency-bound phases (the
+    one-grid-barrier-per-column tridiagonalisation holds every SM at ~1/3
+    issue) leave room for the other lane's GEMMs, colour pass and quantiser,
+    and each solve's host-side waits (convergence trace, eigen-solver checks)
+    block only its own thread. Lanes persist for the process so their
+    contexts, arenas and Ozaki caches are reused across calls."""
 
-    ``stacks``: (V, E, H, W, 3) uint8 host tensors/arrays of one shape (pinned
-    torch tensors give truly asynchronous copies). The u8 images go through two
-    device slots on a copy stream; the solve, quantiser and the D2H of each
-    stack's quantised levels run on the current stream. Returns one
-    ``StackResult`` per stack (levels, step, trace, relative error; no model).
-    This is the data-parallel unit of work: ``dist.assign_stacks`` gives each
-    rank its stack ids and every rank calls this on its own share, with no
-    inter-GPU traffic (the reference's analogue is its process pool over
-    independent cells, cli.py:379-382).
-    """
+    def __init__(self, device: int):
+        import queue
+        import threading
+
+        self.device = device
+        self.q: "queue.Queue" = queue.Queue()
+        self.state: dict = {}
+        self.ready = threading.Event()
+        self.thread = threading.Thread(target=self._run, name=f"tmb-lane-{device}", daemon=True)
+        self.thread.start()
+        self.ready.wait()
+
+    def _run(self) -> None:
+        torch = L._torch()
+        torch.cuda.set_device(self.device)
+        self.stream = torch.cuda.Stream()
+        with torch.cuda.stream(self.stream):
+            self.ctx = L.ctx()
+        self.ready.set()
+        while True:
+            fn, fut = self.q.get()
+            try:
+                with torch.cuda.stream(self.stream):
+                    fut.set_result(fn(self))
+            except BaseException as exc:  # noqa: BLE001 -- re-raised by the caller's result()
+                fut.set_exception(exc)
+
+    def submit(self, fn):
+        import concurrent.futures as cf
+
+        fut = cf.Future()
+        self.q.put((fn, fut))
+        return fut
+
+
+_LANES: dict[int, list[_Lane]] = {}
+
+
+def stream_lanes(count: int) -> list[_Lane]:
+    """The first ``count`` persistent lanes of the current device."""
     torch = L._torch()
-    stacks = [torch.from_numpy(np.ascontiguousarray(s)) if isinstance(s, np.ndarray) else s for s in stacks]
-    if not stacks:
-        return []
-    shape = tuple(stacks[0].shape)
-    for s in stacks:
-        if tuple(s.shape) != shape or s.dtype != torch.uint8:
-            raise ValueError("encode_stacks needs (V, E, H, W, 3) uint8 stacks of one shape")
-    v, e, h, w, _ = shape
-    dims = (h, w, 3, v * e)
-    ranks = tuple(int(r) for r in ranks)
-    cfg = SolveConfig(ranks=ranks, max_sweeps=sweeps, fit_tol=fit_tol, pp_enter_tol=pp_enter_tol)
-    cfg.validate(dims)
-    ncore = int(np.prod(ranks))
+    dev = torch.cuda.current_device()
+    pool = _LANES.setdefault(dev, [])
+    while len(pool) < count:
+        pool.append(_Lane(dev))
+    return pool[:count]
+
+
+DEFAULT_LANES = 2
+
+
+def _encode_seq(stacks, space, ranks, cfg, qp, rel_err, ncore):
+    """The single-stream pipeline on the current stream: the u8 images go
+    through two device slots on a copy stream (H2D of stack i+1 overlaps the
+    solve of stack i); the solve, quantiser and the D2H of each stack's levels
+    run on the current stream."""
+    torch = L._torch()
     comp = torch.cuda.current_stream()
     copy = torch.cuda.Stream()
+    shape = tuple(stacks[0].shape)
     slots = [torch.empty(shape, dtype=torch.uint8, device="cuda") for _ in range(min(2, len(stacks)))]
     loaded = [torch.cuda.Event() for _ in slots]
     freed = [torch.cuda.Event() for _ in slots]
@@ -171,6 +209,87 @@ def encode_stacks(stacks, space: str, ranks: Sequence[int], sweeps: int, qp: int
     comp.synchronize()
     return [StackResult(None, trace, np.reshape(host.numpy(), ranks, order="F"), step, rel)
             for host, trace, step, rel in pending]
+
+
+def encode_stacks(stacks, space: str, ranks: Sequence[int], sweeps: int, qp: int, fit_tol: float = 1e-300,
+                  pp_enter_tol: float = 0.0, rel_err: bool = True, lanes: int | None = None) -> list[StackResult]:
+    """Encode a sequence of independent stacks on this rank's GPU (BASELINE
+    config 3).
+
+    ``stacks``: (V, E, H, W, 3) uint8 host tensors/arrays of one shape (pinned
+    torch tensors give truly asynchronous copies). Stack i goes to lane
+    ``i % lanes`` (``_Lane``: a host thread with its own stream and context;
+    default ``DEFAULT_LANES``), so two solves share the GPU; on each lane the
+    H2D of its next stack overlaps the solve of its current one ("H2D of stack
+    i+1's u8 planes overlaps compute of stack i"). Results are bit-identical
+    to per-stack ``encode_stack`` calls whatever the lane count (every kernel
+    is deterministic and lanes share no device state). Returns one
+    ``StackResult`` per stack, in input order (levels, step, trace, relative
+    error; no model). This is the data-parallel unit of work:
+    ``dist.assign_stacks`` gives each rank its stack ids and every rank calls
+    this on its own share, with no inter-GPU traffic (the reference's analogue
+    is its process pool over independent cells, cli.py:379-382).
+    """
+    torch = L._torch()
+    stacks = [torch.from_numpy(np.ascontiguousarray(s)) if isinstance(s, np.ndarray) else s for s in stacks]
+    if not stacks:
+        return []
+    shape = tuple(stacks[0].shape)
+    for s in stacks:
+        if tuple(s.shape) != shape or s.dtype != torch.uint8:
+            raise ValueError("encode_stacks needs (V, E, H, W, 3) uint8 stacks of one shape")
+    v, e, h, w, _ = shape
+    dims = (h, w, 3, v * e)
+    ranks = tuple(int(r) for r in ranks)
+    cfg = SolveConfig(ranks=ranks, max_sweeps=sweeps, fit_tol=fit_tol, pp_enter_tol=pp_enter_tol)
+    cfg.validate(dims)
+    ncore = int(np.prod(ranks))
+    nl = max(1, min(int(DEFAULT_LANES if lanes is None else lanes), len(stacks)))
+    if nl == 1:
+        return _encode_seq(stacks, space, ranks, cfg, qp, rel_err, ncore)
+    futs = [lane.submit(lambda _l, j=j: _encode_seq(stacks[j::nl], space, ranks, cfg, qp, rel_err, ncore))
+            for j, lane in enumerate(stream_lanes(nl))]
+    parts = [f.result() for f in futs]
+    out: list = [None] * len(stacks)
+    for j, part in enumerate(parts):
+        out[j::nl] = part
+    return out
+
+
+def encode_stacks_device(dev_stacks, space: str, ranks: Sequence[int], cfg: SolveConfig, qp: int,
+                         rel_err: bool = True, lanes: int | None = None) -> list[tuple[SolveTrace, float, float | None]]:
+    """Device-resident form of :func:`encode_stacks` (inputs already in HBM,
+    results left on the device): stack i solves on lane ``i % lanes``, each
+    lane reusing its own device buffers across calls. Ordered after the
+    caller's stream on entry; the caller's stream waits for every lane on
+    exit. Returns (trace, step, rel_err) per stack, in input order."""
+    torch = L._torch()
+    if not dev_stacks:
+        return []
+    ranks = tuple(int(r) for r in ranks)
+    nl = max(1, min(int(DEFAULT_LANES if lanes is None else lanes), len(dev_stacks)))
+    caller = torch.cuda.current_stream()
+    start = torch.cuda.Event()
+    start.record(caller)
+
+    def run(lane, j):
+        lane.stream.wait_event(start)
+        res = []
+        for d in dev_stacks[j::nl]:
+            bufs, tr, step, rel = encode_stack_device(d, space, ranks, cfg, qp, rel_err, lane.state.get("bufs"))
+            lane.state["bufs"] = bufs
+            res.append((_trace_from_c(tr), step, rel))
+        done = torch.cuda.Event()
+        done.record(lane.stream)
+        return res, done
+
+    futs = [lane.submit(lambda ln, j=j: run(ln, j)) for j, lane in enumerate(stream_lanes(nl))]
+    out: list = [None] * len(dev_stacks)
+    for j, f in enumerate(futs):
+        res, done = f.result()
+        caller.wait_event(done)
+        out[j::nl] = res
+    return out
 
 
 # ---------------------------------------------------------------------------

@@ -276,3 +276,29 @@ def test_encode_stacks_batch_equals_per_stack():
         assert np.array_equal(r.levels, one.levels) and r.step == one.step
         assert r.rel_err == one.rel_err
         assert [x.fit for x in r.trace.records] == [x.fit for x in one.trace.records]
+
+
+def test_encode_stacks_lanes_bitwise():
+    """Stacks spread over 1, 2 or 3 concurrent lanes (host threads with their
+    own stream and libtmb context) give bit-identical results in input order,
+    and the device-resident form matches the host form."""
+    import torch
+
+    from paper_2104_04726_b200.pipeline import encode_stacks_device
+
+    cfg = CONFIGS["c3"]
+    stacks = [make_stack(cfg, seed=s, frame=s, height=135, width=240) for s in range(5)]
+    ranks = (17, 30, 3, 5)
+    pinned = [torch.from_numpy(s).pin_memory() for s in stacks]
+    runs = {nl: tb.encode_stacks(pinned, cfg.space, ranks, 3, cfg.qp, lanes=nl) for nl in (1, 2, 3)}
+    for nl in (2, 3):
+        for a, b in zip(runs[1], runs[nl]):
+            assert np.array_equal(a.levels, b.levels) and a.step == b.step and a.rel_err == b.rel_err
+            assert [x.fit for x in a.trace.records] == [x.fit for x in b.trace.records]
+    sc = tb.SolveConfig(ranks=ranks, max_sweeps=3, fit_tol=1e-300, pp_enter_tol=0.0)
+    dev = [p.to("cuda") for p in pinned]
+    res = encode_stacks_device(dev, cfg.space, ranks, sc, cfg.qp, True, 2)
+    torch.cuda.synchronize()
+    for a, (trace, step, rel) in zip(runs[1], res):
+        assert step == a.step and rel == a.rel_err
+        assert [x.fit for x in trace.records] == [x.fit for x in a.trace.records]

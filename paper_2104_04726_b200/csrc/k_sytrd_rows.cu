@@ -35,6 +35,7 @@ struct RowArgs {
   int64_t ld = 0;  // k_sytrd_smem: leading dimension of A and hv (0: n) -- a trailing block of a larger matrix
   int resume = 0;  // k_sytrd_smem: reflector 0 (hv column 0, tau[0]) and d[0], e[0] already computed by
                    // the kernel that ran the earlier steps; A holds rows/columns >= 1 updated through them
+  int scribe = 0;  // k_sytrd_smem: block 0 owns no columns (see the kernel)
 };
 
 __device__ __forceinline__ double frcp(double b) {
@@ -49,6 +50,18 @@ __device__ __forceinline__ double frcp(double b) {
 __device__ __forceinline__ double wsum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Pairwise tree over t[0..M): t[i] += t[i + ceil(M/2)] level by level (for a power
+// of two the halving tree; also valid for 12 warps). Result in t[0].
+template <int M>
+__device__ __forceinline__ void tree_sum(double* t) {
+  if constexpr (M > 1) {
+    constexpr int H = (M + 1) / 2;
+#pragma unroll
+    for (int i = 0; i < M - H; ++i) t[i] += t[i + H];
+    tree_sum<H>(t);
+  }
 }
 
 // Block sum, broadcast; fixed order (8 warps). One barrier per call: the warp
@@ -75,10 +88,7 @@ __device__ __forceinline__ double bsum_get(const double* r) {
     t[i] = q.x;
     t[i + 1] = q.y;
   }
-#pragma unroll
-  for (int h = NW / 2; h > 0; h >>= 1)
-#pragma unroll
-    for (int i = 0; i < h; ++i) t[i] += t[i + h];
+  tree_sum<NW>(t);
   return t[0];
 }
 
@@ -97,10 +107,7 @@ __device__ __forceinline__ double bsum(double v, double* red, int& phase) {
     t[i] = q.x;
     t[i + 1] = q.y;
   }
-#pragma unroll
-  for (int h = NW / 2; h > 0; h >>= 1)
-#pragma unroll
-    for (int i = 0; i < h; ++i) t[i] += t[i + h];  // pairwise tree: depth log2(NW)
+  tree_sum<NW>(t);  // pairwise tree: depth log2(NW)
   return t[0];
 }
 
@@ -324,8 +331,16 @@ __global__ void __launch_bounds__(RW_THREADS, 512 / RW_THREADS) k_sytrd_rows(con
 // blocks read goes to global: p_{k+1} (pbuf) and the column that becomes the
 // next pivot column (k+2), published by its owner during the pass.
 // Same arithmetic, in the same order, as k_sytrd_rows (bitwise identical).
-template <int RPT, int NT, bool PROF>
-__global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, int qmax, long long* prof) {
+//
+// CREG > 0 (register-resident variant): the block's LAST CREG owned columns --
+// the ones that stay live longest -- are kept in REGISTERS (thread t holds its
+// RPT rows of each), only the earlier ones in shared memory (qsm columns). The
+// fused pass is bound by shared-memory bandwidth (one 8-byte load + store per
+// element and step); register columns take that traffic away, and once the
+// shared-memory columns have retired (k > jb + NB qb) the pass touches no
+// memory at all. Same arithmetic and reduction trees per column as CREG = 0.
+template <int RPT, int NT, bool PROF, int CREG = 0, int BPS = 512 / NT>
+__global__ void __launch_bounds__(NT, BPS) k_sytrd_smem(const RowArgs a, int qmax, int qsm, long long* prof) {
   long long t_[10];
 #define SM_T(ix) if constexpr (PROF) t_[ix] = clock64();
   constexpr int NW = NT / 32;
@@ -334,17 +349,22 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
   const int64_t n = a.n;
   const int64_t ld = a.ld ? a.ld : a.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int NB = gridDim.x, b = blockIdx.x;
+  // scribe mode: block 0 owns no columns -- it only does the redundant per-step work and
+  // the stores of the reflectors / d / e / tau, which otherwise make it the last block
+  // at every grid barrier; blocks 1.. share the columns
+  const int blk = blockIdx.x;
+  const int NB = a.scribe ? (int)gridDim.x - 1 : (int)gridDim.x;  // column-owning blocks
+  const int b = a.scribe ? blk - 1 : blk;                         // owner index (-1: the scribe)
   double* A = a.A;
   extern __shared__ double sm[];
   double* cols = sm;                          // qmax x N, column q = jb + NB q
-  double* part = cols + ((size_t)qmax * N + 1) / 2 * 2;  // NW x qmax per-warp partial dots (16-B aligned)
+  double* part = cols + ((size_t)qsm * N + 1) / 2 * 2;   // NW x qmax per-warp partial dots (16-B aligned)
   double* red = part + NW * qmax;             // 2 x NW
   double* vo = red + 2 * NW;                  // qmax: v_k at the owned column indices
   double* wo = vo + qmax;                     // qmax: w_k at the owned column indices
   double* piv = wo + qmax;                    // [0] = v_k[k+2]
   int rph = 0;
-  const int jb = b >= 1 ? b : b + NB;         // column 0 is only read (reflector 0)
+  const int jb = b < 0 ? N : (b >= 1 ? b : b + NB);  // column 0 is only read (reflector 0)
   const int nown = jb < N ? (N - 1 - jb) / NB + 1 : 0;
   int qi[RPT];                                // slot of row i if i is an owned column index
 #pragma unroll
@@ -352,9 +372,24 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
     const int i = tid + NT * u;
     qi[u] = (i >= jb && i < N && (i - jb) % NB == 0) ? (i - jb) / NB : -1;
   }
-  for (int q = 0; q < nown; ++q) {
+  // slots [0, qb) live in shared memory, slots qb + r (r < nreg <= CREG) in registers
+  const int qb = CREG > 0 ? (nown > CREG ? nown - CREG : 0) : nown;
+  const int nreg = nown - qb;
+  for (int q = 0; q < qb; ++q) {
     const double* src = A + ld * (jb + (int64_t)NB * q);
     for (int i = tid; i < N; i += NT) cols[q * N + i] = src[i];
+  }
+  double ar[(CREG > 0 ? CREG : 1) * RPT];
+  if constexpr (CREG > 0) {
+#pragma unroll
+    for (int r = 0; r < CREG; ++r) {
+      const double* src = A + ld * (jb + (int64_t)NB * (qb + (r < nreg ? r : 0)));
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int i = tid + NT * u;
+        ar[r * RPT + u] = (r < nreg && i < N) ? src[i] : 0.0;
+      }
+    }
   }
 
   double vr[RPT], wr[RPT], nr[RPT];
@@ -391,7 +426,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
       if (qi[u] >= 0) vo[qi[u]] = vr[u];
       if (i == 2) piv[0] = vr[u];
     }
-  } else if (b == 0) {
+  } else if (blk == 0) {
     if (tid == 0) { a.d[0] = A[0]; a.e[0] = beta; a.tau[0] = tau_k; }
 #pragma unroll
     for (int u = 0; u < RPT; ++u) {
@@ -401,7 +436,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
   }
   __syncthreads();
   // p_0 = tau_0 A v_0 on owned columns (no update yet)
-  for (int q = 0; q < nown; ++q) {
+  for (int q = 0; q < qb; ++q) {
     double acc = 0.0;
 #pragma unroll
     for (int u = 0; u < RPT; ++u) {
@@ -411,6 +446,22 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
     }
     acc = wsum(acc);
     if (lane == 0) part[warp * qmax + q] = acc;
+  }
+  if constexpr (CREG > 0) {
+#pragma unroll
+    for (int r = 0; r < CREG; ++r) {
+      if (r < nreg) {
+        double acc = 0.0;
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+          const int i = tid + NT * u;
+          const double cv = (i >= 1 && i < N) ? ar[r * RPT + u] : 0.0;
+          acc = fma(cv, vr[u], acc);
+        }
+        acc = wsum(acc);
+        if (lane == 0) part[warp * qmax + qb + r] = acc;
+      }
+    }
   }
   __syncthreads();
   if (tid < nown) {
@@ -453,7 +504,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
       if (i >= k + 3 && i < N) s2 = fma(xa[u], xa[u], s2);
     }
     if (k + 3 == n) {
-      if (b == 0) {
+      if (blk == 0) {
 #pragma unroll
         for (int u = 0; u < RPT; ++u) {
           const int i = tid + NT * u;
@@ -495,7 +546,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
       const int i = tid + NT * u;
       nr[u] = i == k + 2 ? 1.0 : (i >= k + 3 && i < N ? xa[u] * scale : 0.0);
     }
-    if (b == 0) {
+    if (blk == 0) {
       if (tid == 0) { a.e[c1] = beta; a.tau[c1] = tau_n; }
       double* h = a.hv + ld * c1;
 #pragma unroll
@@ -518,12 +569,12 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
     for (int u = 0; u < RPT; ++u) lv[u] = tid + NT * u >= k2 && tid + NT * u < N;
     const int qpub = (k2 - jb) % NB == 0 && k2 >= jb ? (k2 - jb) / NB : -1;
     const int qlast = (k2 + 2 == N && (N - 1 - jb) % NB == 0 && N - 1 >= jb) ? (N - 1 - jb) / NB : -1;
-    for (int q = q0; q < nown; q += 4) {
+    for (int q = q0; q < qb; q += 4) {
       double acc[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         acc[c] = 0.0;
-        if (q + c < nown) {
+        if (q + c < qb) {
           const double vj = vo[q + c], wj = wo[q + c];
           double* cq = cols + (q + c) * N + tid;
 #pragma unroll
@@ -544,16 +595,77 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
       t += __shfl_xor_sync(0xffffffffu, t, 2);
       t += __shfl_xor_sync(0xffffffffu, t, 1);
       const int cs = (up ? 2 : 0) + (up2 ? 1 : 0);  // column slot this lane's sum belongs to
-      if ((lane & 7) == 0 && q + cs < nown) part[warp * qmax + q + cs] = t;
+      if ((lane & 7) == 0 && q + cs < qb) part[warp * qmax + q + cs] = t;
+    }
+    if constexpr (CREG > 0) {
+      // register-resident columns, four per group (static register indices; the
+      // group / column guards are block-uniform)
+#pragma unroll
+      for (int g = 0; g < CREG; g += 4) {
+        if (g < nreg && qb + g + 3 >= q0) {
+        double acc[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          acc[c] = 0.0;
+          if (g + c < CREG) {
+            const int r = g + c < CREG ? g + c : 0;
+            if (g + c < nreg && qb + g + c >= q0) {
+              const double vj = vo[qb + g + c], wj = wo[qb + g + c];
+#pragma unroll
+              for (int u = 0; u < RPT; ++u) {
+                if (lv[u]) {
+                  const double xv = ar[r * RPT + u] - vr[u] * wj - wr[u] * vj;
+                  ar[r * RPT + u] = xv;
+                  acc[c] = fma(xv, nr[u], acc[c]);
+                }
+              }
+            }
+          }
+        }
+        const bool up = lane & 16, up2 = lane & 8;
+        const double r0 = (up ? acc[2] : acc[0]) + __shfl_xor_sync(0xffffffffu, up ? acc[0] : acc[2], 16);
+        const double r1 = (up ? acc[3] : acc[1]) + __shfl_xor_sync(0xffffffffu, up ? acc[1] : acc[3], 16);
+        double t = (up2 ? r1 : r0) + __shfl_xor_sync(0xffffffffu, up2 ? r0 : r1, 8);
+        t += __shfl_xor_sync(0xffffffffu, t, 4);
+        t += __shfl_xor_sync(0xffffffffu, t, 2);
+        t += __shfl_xor_sync(0xffffffffu, t, 1);
+        const int cs = (up ? 2 : 0) + (up2 ? 1 : 0);
+        if ((lane & 7) == 0 && g + cs < nreg && qb + g + cs >= q0) part[warp * qmax + qb + g + cs] = t;
+        }
+      }
     }
     // publish the next pivot column (and, before the last step, the last diagonal)
     if (qpub >= q0 && qpub >= 0 && qpub < nown) {
       double* gq = A + ld * k2;
+      if (qpub < qb) {
 #pragma unroll
-      for (int u = 0; u < RPT; ++u)
-        if (lv[u]) gq[tid + NT * u] = cols[qpub * N + tid + NT * u];
+        for (int u = 0; u < RPT; ++u)
+          if (lv[u]) gq[tid + NT * u] = cols[qpub * N + tid + NT * u];
+      } else if constexpr (CREG > 0) {
+        // selects, not an if-chain on the slot: alternative branches with the
+        // same body get merged into one with a dynamic (local-memory) index
+        const int rp = qpub - qb;
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+          double xv = ar[u];
+#pragma unroll
+          for (int r = 1; r < CREG; ++r) xv = rp == r ? ar[r * RPT + u] : xv;
+          if (lv[u]) gq[tid + NT * u] = xv;
+        }
+      }
     }
-    if (qlast >= 0 && qlast < nown && tid == (N - 1) % NT) A[(n - 1) + ld * (n - 1)] = cols[qlast * N + N - 1];
+    if (qlast >= 0 && qlast < nown && tid == (N - 1) % NT) {
+      if (qlast < qb) A[(n - 1) + ld * (n - 1)] = cols[qlast * N + N - 1];
+      else if constexpr (CREG > 0) {
+        const int rl = qlast - qb;
+        double xv = 0.0;
+#pragma unroll
+        for (int r = 0; r < CREG; ++r)
+#pragma unroll
+          for (int u = 0; u < RPT; ++u) xv = (rl == r && tid + NT * u == N - 1) ? ar[r * RPT + u] : xv;
+        A[(n - 1) + ld * (n - 1)] = xv;
+      }
+    }
     SM_T(6);
     __syncthreads();
     SM_T(7);
@@ -563,10 +675,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
       double t[NW];
 #pragma unroll
       for (int w = 0; w < NW; ++w) t[w] = part[w * qmax + tid];
-#pragma unroll
-      for (int h = NW / 2; h > 0; h >>= 1)
-#pragma unroll
-        for (int w = 0; w < h; ++w) t[w] += t[w + h];
+      tree_sum<NW>(t);
       pbn[jb + (int64_t)NB * tid] = tau_n * t[0];
     }
 #pragma unroll
@@ -579,20 +688,34 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_sytrd_smem(const RowArgs a, in
     tau_k = tau_n;
     SM_T(8);
     grid.sync();
-    if (PROF && tid == 0 && (b == 0 || b == NB / 2)) {
+    if (PROF && tid == 0 && (blk == 0 || blk == (int)gridDim.x / 2)) {
       SM_T(9);
-      long long* r = prof + ((b ? 1 : 0) * 4 + (int)(4 * k / n)) * 10;
+      long long* r = prof + ((blk ? 1 : 0) * 4 + (int)(4 * k / n)) * 10;
       for (int ph = 0; ph < 9; ++ph) atomicAdd((unsigned long long*)(r + ph), (unsigned long long)(t_[ph + 1] - t_[ph]));
       atomicAdd((unsigned long long*)(r + 9), 1ull);
     }
   }
 #undef SM_T
   if (k + 2 < n) {  // stopped at k_end: the trailing block (rows/columns > k) continues from global memory
-    for (int q = 0; q < nown; ++q) {
+    for (int q = 0; q < qb; ++q) {
       const int64_t j = jb + (int64_t)NB * q;
       if (j <= k) continue;
       double* dst = A + ld * j;
       for (int i = (int)k + 1 + tid; i < N; i += NT) dst[i] = cols[q * N + i];
+    }
+    if constexpr (CREG > 0) {
+#pragma unroll
+      for (int r = 0; r < CREG; ++r) {
+        const int64_t j = jb + (int64_t)NB * (qb + r);
+        if (r < nreg && j > k) {
+          double* dst = A + ld * j;
+#pragma unroll
+          for (int u = 0; u < RPT; ++u) {
+            const int i = tid + NT * u;
+            if (i >= (int)k + 1 && i < N) dst[i] = ar[r * RPT + u];
+          }
+        }
+      }
     }
   }
 }
@@ -611,8 +734,18 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
     const char* s = std::getenv("TMB_SMEM_BPS");  // A/B: blocks per SM
     return s ? std::atoi(s) : 0;
   }();
-  const int nt = nt_env ? nt_env : 512;
-  const int bps = bps_env ? bps_env : (nt == 256 ? 2 : 1);
+  static const int creg_env = [] {
+    const char* s = std::getenv("TMB_SMEM_CREG");  // A/B: register-resident columns per block (0: none)
+    return s ? std::atoi(s) : -1;
+  }();
+  // default (measured, scripts/gpu_s5_creg.sh): ONE 256-thread block per SM with the last 4
+  // owned columns in registers -- n = 1080: 4.11 -> 3.56 ms, n = 1920: 8.45 -> 8.00 ms against
+  // the 512-thread blocks (fewer warps shorten every block reduction on the step's serial
+  // path; the register columns take the rest). TMB_SMEM_NT=512 restores the old shape.
+  const int creg = creg_env >= 0 ? creg_env : 4;
+  const int nt = nt_env ? nt_env : 256;
+  const bool regvar = nt != 512 && !(nt == 256 && bps_env == 2);  // one block per SM, up to 255 registers
+  const int bps = bps_env ? bps_env : 1;
   static const int nb_env = [] {
     const char* s = std::getenv("TMB_SMEM_NB");  // A/B: grid size (blocks)
     return s ? std::atoi(s) : 0;
@@ -620,12 +753,47 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
   const int nb = nb_env > 0 ? std::min(nb_env, bps * c.num_sms) : bps * c.num_sms;
   const int rpt = (int)ceil_div(n, nt);
   static const bool rpt4_env = std::getenv("TMB_SMEM_RPT4") != nullptr;  // A/B: 4 rows/thread for n <= 1536
-  using KFn = void (*)(RowArgs, int, long long*);
+  using KFn = void (*)(RowArgs, int, int, long long*);
   KFn kern = nullptr;
-  const int qmax = (int)ceil_div(n - 1, nb);
+  static const int scribe_env = [] {
+    const char* s = std::getenv("TMB_SMEM_SCRIBE");  // A/B: block 0 stores the reflectors and owns no columns
+    return s ? std::atoi(s) : -1;
+  }();
+  const int scribe = scribe_env >= 0 ? (scribe_env != 0) : 0;
+  const int qmax = (int)ceil_div(n - 1, nb - scribe);
   static const bool prof_on = std::getenv("TMB_TRD_PROFILE") != nullptr;
 #define SMEM_K(R, T) (prof_on ? k_sytrd_smem<R, T, true> : k_sytrd_smem<R, T, false>)
-  if (nt == 512) {
+#define SMEM_KR(R, T, C) (prof_on ? k_sytrd_smem<R, T, true, C, 1> : k_sytrd_smem<R, T, false, C, 1>)
+  int cr = 0;  // register-resident columns of the chosen instantiation
+  if (regvar && nt == 256) {
+    cr = creg >= 8 ? 8 : creg >= 6 ? 6 : creg >= 4 ? 4 : creg >= 2 ? 2 : 0;
+#define SMEM_PICK(R) (cr == 8 ? SMEM_KR(R, 256, 8) : cr == 6 ? SMEM_KR(R, 256, 6) : cr == 4 ? SMEM_KR(R, 256, 4) \
+                      : cr == 2 ? SMEM_KR(R, 256, 2) : SMEM_KR(R, 256, 0))
+#define SMEM_PICK4(R) (cr = std::min(cr, 4), cr == 4 ? SMEM_KR(R, 256, 4) : SMEM_KR(R, 256, 0))
+    if (rpt <= 3) { kern = SMEM_PICK4(3); }
+    else if (rpt <= 4) { kern = SMEM_PICK4(4); }
+    else if (rpt <= 5) { kern = SMEM_PICK(5); }
+    else if (rpt <= 6) { kern = SMEM_PICK4(6); }
+    else if (rpt <= 7) { kern = SMEM_PICK4(7); }
+    else if (rpt <= 8) { kern = SMEM_PICK(8); }
+#undef SMEM_PICK
+#undef SMEM_PICK4
+    if (cr == 2 && rpt != 5 && rpt != 8) cr = 0;
+  } else if (regvar && nt == 128) {
+    cr = creg >= 2 ? 2 : 0;
+#define SMEM_PICK(R) (cr == 2 ? SMEM_KR(R, 128, 2) : SMEM_KR(R, 128, 0))
+    if (rpt <= 6) { kern = SMEM_PICK(6); }
+    else if (rpt <= 9) { kern = SMEM_PICK(9); }
+    else if (rpt <= 12) { kern = SMEM_PICK(12); }
+    else if (rpt <= 16) { kern = SMEM_PICK(16); }
+#undef SMEM_PICK
+  } else if (regvar && nt == 384) {
+    cr = creg >= 4 ? 4 : creg >= 2 ? 2 : 0;
+#define SMEM_PICK(R) (cr == 4 ? SMEM_KR(R, 384, 4) : cr == 2 ? SMEM_KR(R, 384, 2) : SMEM_KR(R, 384, 0))
+    if (rpt <= 3) { kern = SMEM_PICK(3); }
+    else if (rpt <= 5) { kern = SMEM_PICK(5); }
+#undef SMEM_PICK
+  } else if (nt == 512) {
     if (rpt <= 2) { kern = SMEM_K(2, 512); }
     else if (rpt <= 3 && !rpt4_env) { kern = SMEM_K(3, 512); }  // n <= 1536 (C2 mode 0)
     else if (rpt <= 4) { kern = SMEM_K(4, 512); }
@@ -634,9 +802,11 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
     else if (rpt <= 8) { kern = SMEM_K(8, 256); }
   }
 #undef SMEM_K
+#undef SMEM_KR
   if (!kern) return false;
   const int nw = nt / 32;
-  const size_t smem = sizeof(double) * (((size_t)qmax * n + 1) / 2 * 2 + (size_t)nw * qmax + 2 * nw + 2 * qmax + 1);
+  const int qsm = std::max(qmax - cr, 0);  // shared-memory columns per block
+  const size_t smem = sizeof(double) * (((size_t)qsm * n + 1) / 2 * 2 + (size_t)nw * qmax + 2 * nw + 2 * qmax + 1);
   if (smem > 227 * 1024) return false;
   set_smem_attr(c, (const void*)kern, std::max<size_t>(smem, 48 * 1024));
   if (blocks_per_sm(c, (const void*)kern, nt, smem) < bps) return false;
@@ -646,8 +816,8 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
     prof = alloc<long long>(c, 80);
     TMB_CUDA(cudaMemsetAsync(prof, 0, sizeof(long long) * 80, c.stream));
   }
-  RowArgs ra{A, n, k_end, d, e, tau, hv, pbuf, ld, resume};
-  void* args[] = {&ra, (void*)&qmax, &prof};
+  RowArgs ra{A, n, k_end, d, e, tau, hv, pbuf, ld, resume, scribe};
+  void* args[] = {&ra, (void*)&qmax, (void*)&qsm, &prof};
   TMB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, nb, nt, args, smem, c.stream));
   c.launches++;
   check_launch("k_sytrd_smem");

@@ -822,6 +822,138 @@ __global__ void __launch_bounds__(32 * W) k_bisect_mw(const double* __restrict__
   if (threadIdx.x == 0) vals[jd] = 0.5 * (lo + hi);
 }
 
+// Two-sided Sturm count (the inertia of the twisted factorisation N_r D_r N_r^T of T - x I,
+// Sylvester): the pivots q_0..q_{r-1} of the top-down LDL^T, the pivots u_{r+1}..u_{n-1} of
+// the bottom-up UDU^T and the twist element gamma_r = q_r - e_r^2 / u_{r+1}; the count is the
+// number of negative ones. The two half-length chains run on different warps, so a count's
+// latency -- what bounds the multisection -- is halved. Same pivmin guard as sturm_counts
+// (unguarded fast path with an off-chain flag, then recomputed guarded).
+// DOWN = false: returns q_r, cnt = #{q_i < 0, i < r}; DOWN = true: returns u_{r+1},
+// cnt = #{u_i < 0, i > r}.
+template <bool DOWN>
+__device__ __forceinline__ double half_chain(const double* __restrict__ d, const double* __restrict__ e,
+                                             int64_t n, int64_t r, double x, double pivmin, int& cnt) {
+  double q;
+  bool hit = false;
+  int c = 0;
+  if (!DOWN) {
+    q = d[0] - x;
+    for (int64_t i = 1; i <= r; ++i) {
+      hit |= fabs(q) <= pivmin;
+      c += q < 0.0;
+      const double ei = e[i - 1];
+      q = (d[i] - x) - ei * ei * frcp(q);
+    }
+    if (hit) {
+      q = d[0] - x;
+      c = 0;
+      for (int64_t i = 1; i <= r; ++i) {
+        if (fabs(q) <= pivmin) q = -pivmin;
+        c += q < 0.0;
+        const double ei = e[i - 1];
+        q = (d[i] - x) - ei * ei * frcp(q);
+      }
+    }
+  } else {
+    q = d[n - 1] - x;
+    for (int64_t i = n - 2; i > r; --i) {
+      hit |= fabs(q) <= pivmin;
+      c += q < 0.0;
+      const double ei = e[i];
+      q = (d[i] - x) - ei * ei * frcp(q);
+    }
+    hit |= fabs(q) <= pivmin;
+    if (hit) {
+      q = d[n - 1] - x;
+      c = 0;
+      for (int64_t i = n - 2; i > r; --i) {
+        if (fabs(q) <= pivmin) q = -pivmin;
+        c += q < 0.0;
+        const double ei = e[i];
+        q = (d[i] - x) - ei * ei * frcp(q);
+      }
+      if (fabs(q) <= pivmin) q = -pivmin;
+    }
+    c += q < 0.0;  // u_{r+1} itself
+  }
+  cnt = c;
+  return q;
+}
+
+// 32W-way multisection per eigenvalue with two-sided counts: warps [0, W) run the top-down
+// halves, warps [W, 2W) the bottom-up halves of the same 32W shifts.
+template <int W>
+__global__ void __launch_bounds__(64 * W) k_bisect_tw(const double* __restrict__ d, const double* __restrict__ e,
+                                                      int64_t n, int64_t k, double* __restrict__ vals) {
+  constexpr int NPT = 32 * W;
+  __shared__ unsigned masks[2][W];
+  __shared__ double ubot[2][NPT];
+  __shared__ int cbot[2][NPT];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool down = warp >= W;
+  const int m = (down ? warp - W : warp) * 32 + lane;  // shift index, ascending in m
+  const int64_t jd = blockIdx.x;
+  if (jd >= k) return;
+  const int64_t ja = n - 1 - jd;  // ascending index
+  const int64_t r = n / 2;        // twist row (n >= 3)
+  double gl = 1e308, gu = -1e308, emax2 = 0.0;
+  for (int64_t i = lane; i < n; i += 32) {
+    const double rr = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
+    gl = fmin(gl, d[i] - rr);
+    gu = fmax(gu, d[i] + rr);
+    if (i + 1 < n) emax2 = fmax(emax2, e[i] * e[i]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+    gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+    emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
+  }
+  const double pivmin = DBL_MIN * fmax(1.0, emax2);
+  const double span = fmax(gu - gl, fmax(fabs(gl), fabs(gu)) * DBL_EPSILON);
+  double lo = gl - 2.0 * DBL_EPSILON * span - 2.0 * pivmin;
+  double hi = gu + 2.0 * DBL_EPSILON * span + 2.0 * pivmin;
+  const double er = e[r], er2 = er * er;
+  for (int round = 0; round < 24; ++round) {
+    const double w = hi - lo;
+    if (w <= 2.0 * DBL_EPSILON * fmax(fabs(gl), fabs(gu)) + 4.0 * pivmin) break;
+    const auto shift = [&](int mm) { return lo + w * (double)(mm + 1) / (double)(NPT + 1); };
+    const double x = shift(m);
+    const int buf = round & 1;
+    int c;
+    double q;
+    if (down) {
+      q = half_chain<true>(d, e, n, r, x, pivmin, c);
+      ubot[buf][m] = q;
+      cbot[buf][m] = c;
+    } else {
+      q = half_chain<false>(d, e, n, r, x, pivmin, c);
+    }
+    __syncthreads();  // bottom-up halves published
+    if (!down) {
+      double g = q - er2 * frcp(ubot[buf][m]);
+      if (fabs(g) <= pivmin) g = -pivmin;
+      c += cbot[buf][m] + (g < 0.0);
+      const unsigned above = __ballot_sync(0xffffffffu, c > ja);
+      if (lane == 0) masks[buf][warp] = above;
+    }
+    __syncthreads();  // masks ready (all buffers alternate by round parity)
+    int first = NPT;  // first shift whose count exceeds ja
+#pragma unroll
+    for (int qq = W - 1; qq >= 0; --qq) {
+      const unsigned mq = masks[buf][qq];
+      if (mq) first = qq * 32 + __ffs(mq) - 1;
+    }
+    if (first == NPT) {
+      lo = shift(NPT - 1);  // eigenvalue above the last shift
+    } else {
+      const double xf = shift(first), xp = shift(first > 0 ? first - 1 : 0);
+      hi = xf;
+      if (first > 0) lo = xp;
+    }
+  }
+  if (threadIdx.x == 0) vals[jd] = 0.5 * (lo + hi);
+}
+
 // ------------------------------------------------------------------ twisted factorisation
 // One warp per eigenvalue: lane 0 runs the stationary (top-down) D+ chain while
 // lane 1 runs the progressive (bottom-up) D- chain; the twist index r =
@@ -1946,7 +2078,14 @@ static void bisect_top(Ctx& c, const double* d, const double* e, int64_t n, int6
     const char* s = std::getenv("TMB_BISECT_WARPS");  // A/B: warps per eigenvalue (1, 2, 4)
     return s ? std::atoi(s) : 2;  // measured: 1.15 / 1.25 / 1.37 ms tridiag at n=1920 for 2 / 1 / 4
   }();
-  if (bis_w == 4) k_bisect_mw<4><<<(unsigned)k, 128, 0, c.stream>>>(d, e, n, k, vals);
+  static const int bis_tw = [] {
+    const char* s = std::getenv("TMB_BISECT_TWOSIDED");  // A/B: two-sided (twisted) Sturm counts
+    return s ? std::atoi(s) : 1;
+  }();
+  if (bis_tw && n >= 8) {
+    if (bis_w == 4) k_bisect_tw<4><<<(unsigned)k, 256, 0, c.stream>>>(d, e, n, k, vals);
+    else k_bisect_tw<2><<<(unsigned)k, 128, 0, c.stream>>>(d, e, n, k, vals);
+  } else if (bis_w == 4) k_bisect_mw<4><<<(unsigned)k, 128, 0, c.stream>>>(d, e, n, k, vals);
   else if (bis_w == 2) k_bisect_mw<2><<<(unsigned)k, 64, 0, c.stream>>>(d, e, n, k, vals);
   else k_bisect<<<(unsigned)ceil_div(k, 2), 64, 0, c.stream>>>(d, e, n, k, vals);
   LAUNCHED("k_bisect");

@@ -339,6 +339,11 @@ __global__ void __launch_bounds__(RW_THREADS, 512 / RW_THREADS) k_sytrd_rows(con
 // element and step); register columns take that traffic away, and once the
 // shared-memory columns have retired (k > jb + NB qb) the pass touches no
 // memory at all. Same arithmetic and reduction trees per column as CREG = 0.
+//
+// Measured and removed: a software-pipelined pass (next group's loads issued before the
+// current group's arithmetic, each group's shuffle reduction deferred by one group):
+// n = 1920 12.3 vs 8.2 ms, n = 1080 4.3 vs 3.7 ms -- the pass is bound by shared-memory /
+// MIO throughput (69 % of 128 B/clk with all columns in shared memory), not by its latencies.
 template <int RPT, int NT, bool PROF, int CREG = 0, int BPS = 512 / NT>
 __global__ void __launch_bounds__(NT, BPS) k_sytrd_smem(const RowArgs a, int qmax, int qsm, long long* prof) {
   long long t_[10];
@@ -744,7 +749,8 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
   // path; the register columns take the rest). TMB_SMEM_NT=512 restores the old shape.
   const int creg = creg_env >= 0 ? creg_env : 4;
   const int nt = nt_env ? nt_env : 256;
-  const bool regvar = nt != 512 && !(nt == 256 && bps_env == 2);  // one block per SM, up to 255 registers
+  // (128- and 384-thread blocks measured no better: n = 1920 10.99 / 7.95 ms, n = 1080 3.86 / 3.76 ms)
+  const bool regvar = nt == 256 && bps_env != 2;  // one block per SM, up to 255 registers
   const int bps = bps_env ? bps_env : 1;
   static const int nb_env = [] {
     const char* s = std::getenv("TMB_SMEM_NB");  // A/B: grid size (blocks)
@@ -766,10 +772,10 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
 #define SMEM_KR(R, T, C) (prof_on ? k_sytrd_smem<R, T, true, C, 1> : k_sytrd_smem<R, T, false, C, 1>)
   int cr = 0;  // register-resident columns of the chosen instantiation
   if (regvar && nt == 256) {
-    cr = creg >= 8 ? 8 : creg >= 6 ? 6 : creg >= 4 ? 4 : creg >= 2 ? 2 : 0;
-#define SMEM_PICK(R) (cr == 8 ? SMEM_KR(R, 256, 8) : cr == 6 ? SMEM_KR(R, 256, 6) : cr == 4 ? SMEM_KR(R, 256, 4) \
-                      : cr == 2 ? SMEM_KR(R, 256, 2) : SMEM_KR(R, 256, 0))
-#define SMEM_PICK4(R) (cr = std::min(cr, 4), cr == 4 ? SMEM_KR(R, 256, 4) : SMEM_KR(R, 256, 0))
+    // (2, 6 and 8 register columns measured no better than 4: n = 1920 8.16 / 8.24 / 9.41 vs 7.98 ms)
+    cr = creg >= 4 ? 4 : 0;
+#define SMEM_PICK(R) (cr == 4 ? SMEM_KR(R, 256, 4) : SMEM_KR(R, 256, 0))
+#define SMEM_PICK4(R) SMEM_PICK(R)
     if (rpt <= 3) { kern = SMEM_PICK4(3); }
     else if (rpt <= 4) { kern = SMEM_PICK4(4); }
     else if (rpt <= 5) { kern = SMEM_PICK(5); }
@@ -778,21 +784,6 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
     else if (rpt <= 8) { kern = SMEM_PICK(8); }
 #undef SMEM_PICK
 #undef SMEM_PICK4
-    if (cr == 2 && rpt != 5 && rpt != 8) cr = 0;
-  } else if (regvar && nt == 128) {
-    cr = creg >= 2 ? 2 : 0;
-#define SMEM_PICK(R) (cr == 2 ? SMEM_KR(R, 128, 2) : SMEM_KR(R, 128, 0))
-    if (rpt <= 6) { kern = SMEM_PICK(6); }
-    else if (rpt <= 9) { kern = SMEM_PICK(9); }
-    else if (rpt <= 12) { kern = SMEM_PICK(12); }
-    else if (rpt <= 16) { kern = SMEM_PICK(16); }
-#undef SMEM_PICK
-  } else if (regvar && nt == 384) {
-    cr = creg >= 4 ? 4 : creg >= 2 ? 2 : 0;
-#define SMEM_PICK(R) (cr == 4 ? SMEM_KR(R, 384, 4) : cr == 2 ? SMEM_KR(R, 384, 2) : SMEM_KR(R, 384, 0))
-    if (rpt <= 3) { kern = SMEM_PICK(3); }
-    else if (rpt <= 5) { kern = SMEM_PICK(5); }
-#undef SMEM_PICK
   } else if (nt == 512) {
     if (rpt <= 2) { kern = SMEM_K(2, 512); }
     else if (rpt <= 3 && !rpt4_env) { kern = SMEM_K(3, 512); }  // n <= 1536 (C2 mode 0)

@@ -2233,7 +2233,9 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
       }();
       constexpr int64_t kHandSmem = 2000;
       const int64_t km = n - kHandSmem;
-      const bool hand = hand_off && tail1 && !rows_off && km > 0 && km < K0;
+      // (probe first: once the column kernel has stopped at km the shared-memory kernel must take over)
+      const bool hand = hand_off && tail1 && !rows_off && km > 0 && km < K0 &&
+                        sytrd_smem(c, A + km + n * km, n - km, K0 - km, d, e, tau, hv, pbuf, n, -1);
       ta.k_begin = sytrd_lazy_panels(c, A, n, std::min<int64_t>(hand ? km : K0, n - 3), d, e, tau, hv);
       if (hand) ta.k_end = std::max(km, ta.k_begin);
       TMB_CUDA(cudaLaunchCooperativeKernel(kern, blocks, TRD_THREADS, args, smem, c.stream));
@@ -2245,12 +2247,10 @@ void leading_eigvecs(Ctx& c, const double* g, int64_t n, int64_t k, double* vecs
         const int64_t k1 = ta.k_end, n1 = n - k1;
         TMB_CUDA(cudaMemsetAsync(hv + n * (k1 + 1), 0, sizeof(double) * n * (n - k1 - 1), c.stream));
         handed = sytrd_smem(c, A + k1 + n * k1, n1, K0 - k1, d + k1, e + k1, tau + k1, hv + k1 + n * k1, pbuf, n, 1);
-        if (!handed) {  // did not fit after all: the column kernel finishes from k1
-          ta.k_begin = k1;
-          ta.k_end = K0;
-          TMB_CUDA(cudaLaunchCooperativeKernel(kern, blocks, TRD_THREADS, args, smem, c.stream));
-          LAUNCHED("k_sytrd");
-        }
+        // the probe above said it fits; restarting the column kernel at k1 (reflector k1
+        // already formed) measured WRONG eigenvalues (5.6e-3) when a variant did not fit, so
+        // there is no silent fallback here
+        if (!handed) throw Error(TMB_ECUDA, "sytrd: the shared-memory kernel refused the hand-off block");
       }
     }
     if (tail1) sytrd_tail1(c, A, n, K0, d, e, tau, hv);

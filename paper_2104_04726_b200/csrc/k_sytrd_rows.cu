@@ -502,13 +502,10 @@ __global__ void __launch_bounds__(NT, BPS) k_sytrd_smem(const RowArgs a, int qma
     SM_T(2);
     const double v_c1 = 1.0, v_k2 = piv[0];  // v_k[k+1] = 1 by construction
     const double w_c1 = p_c1 - K * v_c1, w_k2 = p_k2 - K * v_k2;
-    s2 = 0.0;
 #pragma unroll
     for (int u = 0; u < RPT; ++u) {
-      const int i = tid + NT * u;
       wr[u] = pp[u] - K * vr[u];
       xa[u] = xa[u] - vr[u] * w_c1 - wr[u] * v_c1;
-      if (i >= k + 3 && i < N) s2 = fma(xa[u], xa[u], s2);
     }
     if (k + 3 == n) {
       if (blk == 0) {
@@ -525,6 +522,26 @@ __global__ void __launch_bounds__(NT, BPS) k_sytrd_smem(const RowArgs a, int qma
       }
       break;
     }
+    // x is zero at rows < k+1 and >= N already (v_k, w_k and the gathered column are zero
+    // there); the two rows that must not count in ||x||^2 -- k+1 (the new diagonal entry,
+    // kept in x_c1 by its owner) and k+2 (alpha) -- are zeroed by the ONE thread that holds
+    // each, in a rarely taken branch, so the sums below need no per-row predicates (the
+    // per-row tests cost ~45 + ~65 instructions per warp and step in the ncu source view)
+    static_assert((NT & (NT - 1)) == 0, "row ownership tests assume a power-of-two block");
+    const int d1 = c1 - tid, d2 = d1 + 1;
+    const bool own1 = d1 >= 0 && (d1 & (NT - 1)) == 0, own2 = d2 >= 0 && (d2 & (NT - 1)) == 0;
+    double x_c1 = 0.0;
+    if (own1 || own2) {
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int i = tid + NT * u;
+        if (i == c1) { x_c1 = xa[u]; xa[u] = 0.0; }
+        if (i == c1 + 1) xa[u] = 0.0;
+      }
+    }
+    s2 = 0.0;
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) s2 = fma(xa[u], xa[u], s2);
     // w_k at the owned indices and the warp partials of ||x||^2 are published
     // behind ONE block barrier (the pass needs wo; every thread then forms
     // ||x||^2 from the partials in bsum's fixed order)
@@ -549,18 +566,20 @@ __global__ void __launch_bounds__(NT, BPS) k_sytrd_smem(const RowArgs a, int qma
     }
     SM_T(4);
 #pragma unroll
-    for (int u = 0; u < RPT; ++u) {
-      const int i = tid + NT * u;
-      nr[u] = i == k + 2 ? 1.0 : (i >= k + 3 && i < N ? xa[u] * scale : 0.0);
+    for (int u = 0; u < RPT; ++u) nr[u] = __fma_rn(xa[u], scale, 0.0);  // + 0.0: no -0 at the zero rows
+    if (own2) {
+#pragma unroll
+      for (int u = 0; u < RPT; ++u)
+        if (tid + NT * u == c1 + 1) nr[u] = 1.0;
     }
     if (blk == 0) {
       if (tid == 0) { a.e[c1] = beta; a.tau[c1] = tau_n; }
+      if (own1) a.d[c1] = x_c1;
       double* h = a.hv + ld * c1;
 #pragma unroll
       for (int u = 0; u < RPT; ++u) {
         const int i = tid + NT * u;
         if (i < N) h[i] = nr[u];
-        if (i == c1) a.d[c1] = xa[u];
       }
     }
     SM_T(5);

@@ -292,6 +292,17 @@ __device__ __forceinline__ uint64_t sdesc_sw32(uint32_t addr) {
   return d;
 }
 
+// One elected lane of a CONVERGED warp. The tcgen05 / TMA issue code runs under this
+// predicate instead of `lane == 0`: in a plain divergent branch ptxas wraps every uniform-
+// datapath instruction (UTCIMMA, UTMALDG) in an ELECT / BRA.U.ANY loop over the active
+// lanes -- ~7 dependent instructions and a branch per MMA, 69 cycles per MMA issued against
+// the 34 the tensor pipe needs (ncu source view: the issuing thread 70 % in that loop).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   for (long long it = 0; it < 2000000000LL; ++it) {
     uint32_t done;
@@ -389,7 +400,7 @@ __global__ void __launch_bounds__(OZ_NT, 1) k_oz_gemm(const __grid_constant__ CU
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
 
-  if (warp == 0 && lane == 0) {  // TMA producer: all 8 digit planes of A and of B per K chunk
+  if (warp == 0 && elect_one()) {  // TMA producer: all 8 digit planes of A and of B per K chunk
     for (int kt = 0; kt < KT; ++kt) {
       const int st = kt % OZ_ST;
       if (kt >= OZ_ST) mbar_wait(saddr(&empty[st]), ((kt / OZ_ST) - 1) & 1);
@@ -403,7 +414,7 @@ __global__ void __launch_bounds__(OZ_NT, 1) k_oz_gemm(const __grid_constant__ CU
           "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
           ::"r"(db), "l"(&tb), "r"(kt * OZ_BK), "r"((int)n0), "r"(0), "r"(fb) : "memory");
     }
-  } else if (warp == 1 && lane == 0) {  // MMA issuer: 36 digit pairs x 2 K-halves per chunk
+  } else if (warp == 1 && elect_one()) {  // MMA issuer: 36 digit pairs x 2 K-halves per chunk
     const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_BN >> 3) << 17) |
                            ((uint32_t)(OZ_BM >> 4) << 24);
     for (int kt = 0; kt < KT; ++kt) {
@@ -548,7 +559,7 @@ __global__ void __launch_bounds__(OZ2_NT, 1) k_oz_gemm2(const __grid_constant__ 
   const int NQ = 3 * KT;  // chunk sequence: hi-1 (KT), hi-2 (KT), lo (KT)
 
   if (warp == 4) {
-    if (lane == 0) {  // TMA producer
+    if (elect_one()) {  // TMA producer
       for (int q = 0; q < NQ; ++q) {
         const int ph = q / KT, kt = q % KT, st = q % OZ2_ST;
         if (q >= OZ2_ST) mbar_wait(saddr(&empty[st]), ((q / OZ2_ST) - 1) & 1);
@@ -571,7 +582,7 @@ __global__ void __launch_bounds__(OZ2_NT, 1) k_oz_gemm2(const __grid_constant__ 
       }
     }
   } else if (warp == 5) {
-    if (lane == 0) {  // MMA issuer
+    if (elect_one()) {  // MMA issuer
       const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ2_BN >> 3) << 17) |
                              ((uint32_t)(OZ_BM >> 4) << 24);
       const auto mma = [&](uint32_t col, uint64_t ad, uint64_t bd, uint32_t acc) {

@@ -709,10 +709,16 @@ __global__ void __launch_bounds__(NT, BPS) k_sytrd_smem(const RowArgs a, int qma
     }
 #pragma unroll
     for (int u = 0; u < RPT; ++u) {
-      const int i = tid + NT * u;
       vr[u] = nr[u];
       if (qi[u] >= 0) vo[qi[u]] = nr[u];
-      if (i == k + 3) piv[0] = nr[u];
+    }
+    {  // v_{k+1}[k+3] for the next step, from the one thread that holds row k+3
+      const int d3 = d2 + 1;
+      if (d3 >= 0 && (d3 & (NT - 1)) == 0) {
+#pragma unroll
+        for (int u = 0; u < RPT; ++u)
+          if (tid + NT * u == c1 + 2) piv[0] = nr[u];
+      }
     }
     tau_k = tau_n;
     SM_T(8);

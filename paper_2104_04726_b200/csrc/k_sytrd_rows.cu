@@ -18,6 +18,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "tmb_internal.cuh"
 
@@ -344,7 +345,15 @@ __global__ void __launch_bounds__(RW_THREADS, 512 / RW_THREADS) k_sytrd_rows(con
 // current group's arithmetic, each group's shuffle reduction deferred by one group):
 // n = 1920 12.3 vs 8.2 ms, n = 1080 4.3 vs 3.7 ms -- the pass is bound by shared-memory /
 // MIO throughput (69 % of 128 B/clk with all columns in shared memory), not by its latencies.
-template <int RPT, int NT, bool PROF, int CREG = 0, int BPS = 512 / NT>
+//
+// UBS: the pass specialised on the block-uniform count ub = k2 / NT of row groups u that are
+// dead for EVERY thread (row i = tid + NT u): variant J runs u = J .. RPT-1 as straight-line
+// code with NO per-row predicates (only the last u keeps the beyond-the-matrix guard). Rows
+// of group u = J that are already dead are processed anyway: they have v = w = 0 (unchanged)
+// or are row k+1 (finite junk nobody reads), and v_{k+1} = 0 there, so the dot products are
+// unchanged. The predicated form keeps the RPT row predicates in general registers (there are
+// 7 predicate registers) and re-tests one per element: as many ISETP as DFMA in the ncu mix.
+template <int RPT, int NT, bool PROF, int CREG = 0, int BPS = 512 / NT, int UBS = 0>
 __global__ void __launch_bounds__(NT, BPS) k_sytrd_smem(const RowArgs a, int qmax, int qsm, long long* prof) {
   long long t_[10];
 #define SM_T(ix) if constexpr (PROF) t_[ix] = clock64();
@@ -598,6 +607,88 @@ __global__ void __launch_bounds__(NT, BPS) k_sytrd_smem(const RowArgs a, int qma
     for (int u = 0; u < RPT; ++u) lv[u] = tid + NT * u >= k2 && tid + NT * u < N;
     const int qpub = jq0 == k2 ? q0 : -1;            // slot of column k2 if this block owns it
     const int qlast = k2 + 2 == N ? qlast_own : -1;  // slot of column N - 1 before the last step
+    // ub: row groups dead for every thread of the block (block-uniform)
+    const int ub = k2 / NT;
+    const bool padok = tid + NT * (RPT - 1) < N;
+    bool ubs_done = false;
+    if constexpr (UBS) {
+      const bool up = lane & 16, up2 = lane & 8;
+      const int cs = (up ? 2 : 0) + (up2 ? 1 : 0);  // column slot this lane's sum belongs to
+      auto pass_from = [&](auto jc) {
+        constexpr int J = decltype(jc)::value;
+        for (int q = q0; q < qb; q += 4) {
+          double acc[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            acc[c] = 0.0;
+            if (q + c < qb) {
+              const double vj = vo[q + c], wj = wo[q + c];
+              double* cq = cols + (q + c) * N + tid;
+#pragma unroll
+              for (int u = J; u < RPT; ++u) {
+                if (u < RPT - 1 || padok) {
+                  const double xv = cq[NT * u] - vr[u] * wj - wr[u] * vj;
+                  cq[NT * u] = xv;
+                  acc[c] = fma(xv, nr[u], acc[c]);
+                }
+              }
+            }
+          }
+          const double r0 = (up ? acc[2] : acc[0]) + __shfl_xor_sync(0xffffffffu, up ? acc[0] : acc[2], 16);
+          const double r1 = (up ? acc[3] : acc[1]) + __shfl_xor_sync(0xffffffffu, up ? acc[1] : acc[3], 16);
+          double t = (up2 ? r1 : r0) + __shfl_xor_sync(0xffffffffu, up2 ? r0 : r1, 8);
+          t += __shfl_xor_sync(0xffffffffu, t, 4);
+          t += __shfl_xor_sync(0xffffffffu, t, 2);
+          t += __shfl_xor_sync(0xffffffffu, t, 1);
+          if ((lane & 7) == 0 && q + cs < qb) part[warp * qmax + q + cs] = t;
+        }
+        if constexpr (CREG > 0) {
+#pragma unroll
+          for (int g = 0; g < CREG; g += 4) {
+            if (g < nreg && qb + g + 3 >= q0) {
+              double acc[4];
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                acc[c] = 0.0;
+                if (g + c < CREG) {
+                  const int r = g + c < CREG ? g + c : 0;
+                  if (g + c < nreg && qb + g + c >= q0) {
+                    const double vj = vo[qb + g + c], wj = wo[qb + g + c];
+#pragma unroll
+                    for (int u = J; u < RPT; ++u) {  // rows beyond the matrix hold zeros and have v = w = 0
+                      const double xv = ar[r * RPT + u] - vr[u] * wj - wr[u] * vj;
+                      ar[r * RPT + u] = xv;
+                      acc[c] = fma(xv, nr[u], acc[c]);
+                    }
+                  }
+                }
+              }
+              const double r0 = (up ? acc[2] : acc[0]) + __shfl_xor_sync(0xffffffffu, up ? acc[0] : acc[2], 16);
+              const double r1 = (up ? acc[3] : acc[1]) + __shfl_xor_sync(0xffffffffu, up ? acc[1] : acc[3], 16);
+              double t = (up2 ? r1 : r0) + __shfl_xor_sync(0xffffffffu, up2 ? r0 : r1, 8);
+              t += __shfl_xor_sync(0xffffffffu, t, 4);
+              t += __shfl_xor_sync(0xffffffffu, t, 2);
+              t += __shfl_xor_sync(0xffffffffu, t, 1);
+              if ((lane & 7) == 0 && g + cs < nreg && qb + g + cs >= q0) part[warp * qmax + qb + g + cs] = t;
+            }
+          }
+        }
+      };
+      if (N > NT * (RPT - 1) && ub < RPT) {  // only the last row group may reach beyond the matrix
+        ubs_done = true;
+        switch (ub) {
+          case 0: pass_from(std::integral_constant<int, 0>{}); break;
+          case 1: pass_from(std::integral_constant<int, (RPT > 1 ? 1 : 0)>{}); break;
+          case 2: pass_from(std::integral_constant<int, (RPT > 2 ? 2 : 0)>{}); break;
+          case 3: pass_from(std::integral_constant<int, (RPT > 3 ? 3 : 0)>{}); break;
+          case 4: pass_from(std::integral_constant<int, (RPT > 4 ? 4 : 0)>{}); break;
+          case 5: pass_from(std::integral_constant<int, (RPT > 5 ? 5 : 0)>{}); break;
+          case 6: pass_from(std::integral_constant<int, (RPT > 6 ? 6 : 0)>{}); break;
+          default: pass_from(std::integral_constant<int, (RPT > 7 ? 7 : 0)>{}); break;
+        }
+      }
+    }
+    if (!ubs_done) {
     for (int q = q0; q < qb; q += 4) {
       double acc[4];
 #pragma unroll
@@ -662,6 +753,7 @@ __global__ void __launch_bounds__(NT, BPS) k_sytrd_smem(const RowArgs a, int qma
         if ((lane & 7) == 0 && g + cs < nreg && qb + g + cs >= q0) part[warp * qmax + qb + g + cs] = t;
         }
       }
+    }
     }
     // publish the next pivot column (and, before the last step, the last diagonal)
     if (qpub >= q0 && qpub >= 0 && qpub < nown) {
@@ -800,7 +892,17 @@ bool sytrd_smem(Ctx& c, double* A, int64_t n, int64_t k_end, double* d, double* 
   const int qmax = (int)ceil_div(n - 1, nb - scribe);
   static const bool prof_on = std::getenv("TMB_TRD_PROFILE") != nullptr;
 #define SMEM_K(R, T) (prof_on ? k_sytrd_smem<R, T, true> : k_sytrd_smem<R, T, false>)
-#define SMEM_KR(R, T, C) (prof_on ? k_sytrd_smem<R, T, true, C, 1> : k_sytrd_smem<R, T, false, C, 1>)
+  static const int ubs_env = [] {
+    const char* s = std::getenv("TMB_SMEM_UBS");  // A/B: predicate-free pass variants (see the kernel)
+    return s ? std::atoi(s) : 1;
+  }();
+  // measured (scripts/gpu_s5_ubs.sh): the predicate-free variants win only at 8 rows per thread
+  // (n = 1920: 7.27 -> 7.17 ms; n = 1080: 3.34 -> 3.40 ms, n = 1500: 5.01 -> 5.09 ms), so only
+  // that shape is instantiated with them
+#define SMEM_KR(R, T, C)                                                                                           \
+  (ubs_env && (R) == 8 ? (prof_on ? k_sytrd_smem<R, T, true, C, 1, ((R) == 8 ? 1 : 0)>                             \
+                                  : k_sytrd_smem<R, T, false, C, 1, ((R) == 8 ? 1 : 0)>)                            \
+                       : (prof_on ? k_sytrd_smem<R, T, true, C, 1> : k_sytrd_smem<R, T, false, C, 1>))
   int cr = 0;  // register-resident columns of the chosen instantiation
   if (regvar && nt == 256) {
     // (2, 6 and 8 register columns measured no better than 4: n = 1920 8.16 / 8.24 / 9.41 vs 7.98 ms)

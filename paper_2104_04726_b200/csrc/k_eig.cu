@@ -2074,16 +2074,21 @@ static int64_t sytrd_lazy_panels(Ctx& c, double* A, int64_t n, int64_t k_limit, 
 static void bisect_top(Ctx& c, const double* d, const double* e, int64_t n, int64_t k, double* vals) {
   // 2 warps (eigenvalues) per block: the counts are FP64-throughput bound, so
   // spread the k warps over all SMs (k/8 blocks of 8 warps left 60 % idle)
-  static const int bis_w = [] {
+  static const int bis_w_env = [] {
     const char* s = std::getenv("TMB_BISECT_WARPS");  // A/B: warps per eigenvalue (1, 2, 4)
-    return s ? std::atoi(s) : 2;  // measured: 1.15 / 1.25 / 1.37 ms tridiag at n=1920 for 2 / 1 / 4
+    return s ? std::atoi(s) : 0;  // one-sided counts measured 1.15 / 1.25 / 1.37 ms tridiag at n=1920 for 2 / 1 / 4
   }();
+  // two-sided counts (scripts/gpu_s5_bis.sh, eigenvalue + vector stage): n = 1080, k = 270: 0.34 / 0.31 /
+  // 0.36 ms for 32 / 64 / 128 shifts per round; n = 1920, k = 480: 0.69 / 0.74 / 1.07 ms -- once k n
+  // Sturm chains saturate the FP64 pipes, fewer shifts per round (less total work) win over fewer rounds
+  const int bis_w = bis_w_env ? bis_w_env : (n * k >= 800000 ? 1 : 2);
   static const int bis_tw = [] {
     const char* s = std::getenv("TMB_BISECT_TWOSIDED");  // A/B: two-sided (twisted) Sturm counts
     return s ? std::atoi(s) : 1;
   }();
   if (bis_tw && n >= 8) {
     if (bis_w == 4) k_bisect_tw<4><<<(unsigned)k, 256, 0, c.stream>>>(d, e, n, k, vals);
+    else if (bis_w == 1) k_bisect_tw<1><<<(unsigned)k, 64, 0, c.stream>>>(d, e, n, k, vals);
     else k_bisect_tw<2><<<(unsigned)k, 128, 0, c.stream>>>(d, e, n, k, vals);
   } else if (bis_w == 4) k_bisect_mw<4><<<(unsigned)k, 128, 0, c.stream>>>(d, e, n, k, vals);
   else if (bis_w == 2) k_bisect_mw<2><<<(unsigned)k, 64, 0, c.stream>>>(d, e, n, k, vals);

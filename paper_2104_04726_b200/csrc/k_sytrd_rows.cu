@@ -331,7 +331,8 @@ __global__ void __launch_bounds__(RW_THREADS, 512 / RW_THREADS) k_sytrd_rows(con
 // above spends most of a step in dependent L2 round trips). Only what other
 // blocks read goes to global: p_{k+1} (pbuf) and the column that becomes the
 // next pivot column (k+2), published by its owner during the pass.
-// Same arithmetic, in the same order, as k_sytrd_rows (bitwise identical).
+// Same arithmetic, in the same order, as k_sytrd_rows (bitwise identical for the
+// same block shape; the reduction trees depend on the thread count).
 //
 // CREG > 0 (register-resident variant): the block's LAST CREG owned columns --
 // the ones that stay live longest -- are kept in REGISTERS (thread t holds its
@@ -363,9 +364,9 @@ __global__ void __launch_bounds__(NT, BPS) k_sytrd_smem(const RowArgs a, int qma
   const int64_t n = a.n;
   const int64_t ld = a.ld ? a.ld : a.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // scribe mode: block 0 owns no columns -- it only does the redundant per-step work and
-  // the stores of the reflectors / d / e / tau, which otherwise make it the last block
-  // at every grid barrier; blocks 1.. share the columns
+  // scribe mode (TMB_SMEM_SCRIBE=1, off by default: measured no gain, 8.45 vs 8.45 ms at
+  // n = 1920): block 0 owns no columns -- it only does the redundant per-step work and the
+  // stores of the reflectors / d / e / tau; blocks 1.. share the columns
   const int blk = blockIdx.x;
   const int NB = a.scribe ? (int)gridDim.x - 1 : (int)gridDim.x;  // column-owning blocks
   const int b = a.scribe ? blk - 1 : blk;                         // owner index (-1: the scribe)
